@@ -1,0 +1,63 @@
+# redsynth-b200 build. Everything is compiled in-tree into
+# paper_2110_10548_b200/_lib/ (git-ignored; travels to the GPU box).
+#
+#   make            planner library + synth CLI + CUDA executor library
+#   make oracle     the C oracle and the reference build (oracle/Makefile)
+#   make check-ref  run the reference's own GTest suites against OUR planner
+
+NVCC      ?= /usr/local/cuda/bin/nvcc
+CXX       ?= g++
+PKG       := paper_2110_10548_b200
+LIB       := $(PKG)/_lib
+INC       := -Iinclude -Ithird_party/absl_lite -Ithird_party
+CXXFLAGS  := -std=c++20 -O2 -fPIC -Wall -Wextra -Wno-missing-field-initializers
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   := -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -Wall \
+             --expt-relaxed-constexpr -Xptxas -v
+CUDA_INC  := -I/usr/local/cuda/include
+
+PLANNER_SRCS := $(wildcard $(PKG)/csrc/planner/*.cc)
+PLANNER_OBJS := $(patsubst $(PKG)/csrc/planner/%.cc,$(LIB)/obj/%.o,$(PLANNER_SRCS))
+EXEC_CC      := $(wildcard $(PKG)/csrc/exec/*.cc)
+EXEC_CU      := $(wildcard $(PKG)/csrc/exec/*.cu)
+EXEC_HDRS    := $(wildcard $(PKG)/csrc/exec/*.h) $(wildcard $(PKG)/csrc/exec/*.cuh) \
+                $(wildcard include/*.h) $(wildcard include/redsynth/*.h)
+EXEC_OBJS    := $(patsubst $(PKG)/csrc/exec/%.cc,$(LIB)/obj/exec_%.o,$(EXEC_CC)) \
+                $(patsubst $(PKG)/csrc/exec/%.cu,$(LIB)/obj/cu_%.o,$(EXEC_CU))
+
+.PHONY: all planner exec oracle check-ref clean
+all: planner exec
+
+planner: $(LIB)/libredsynth_planner.a $(LIB)/synth
+
+$(LIB)/obj/%.o: $(PKG)/csrc/planner/%.cc $(wildcard include/redsynth/*.h)
+	@mkdir -p $(LIB)/obj
+	$(CXX) $(CXXFLAGS) $(INC) -c $< -o $@
+
+$(LIB)/libredsynth_planner.a: $(PLANNER_OBJS)
+	ar rcs $@ $^
+
+$(LIB)/synth: $(PKG)/csrc/tools/synth_main.cc $(LIB)/libredsynth_planner.a
+	$(CXX) $(CXXFLAGS) $(INC) -o $@ $< $(LIB)/libredsynth_planner.a -pthread
+
+exec: $(LIB)/libredsynth_b200.so
+
+$(LIB)/obj/exec_%.o: $(PKG)/csrc/exec/%.cc $(EXEC_HDRS)
+	@mkdir -p $(LIB)/obj
+	$(CXX) $(CXXFLAGS) $(INC) $(CUDA_INC) -c $< -o $@
+
+$(LIB)/obj/cu_%.o: $(PKG)/csrc/exec/%.cu $(EXEC_HDRS)
+	@mkdir -p $(LIB)/obj
+	$(NVCC) $(NVFLAGS) $(INC) -c $< -o $@ 2> $(LIB)/obj/cu_$*.ptxas.txt || (cat $(LIB)/obj/cu_$*.ptxas.txt; false)
+
+$(LIB)/libredsynth_b200.so: $(EXEC_OBJS) $(PLANNER_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $^ -Xcompiler -pthread -lcuda
+
+oracle:
+	$(MAKE) -C oracle numeric ref
+
+check-ref: planner
+	$(MAKE) -C oracle mine-tests
+
+clean:
+	rm -rf $(LIB)
