@@ -6,13 +6,13 @@
 #   make check-ref  run the reference's own GTest suites against OUR planner
 
 NVCC      ?= /usr/local/cuda/bin/nvcc
-CXX       ?= g++
+CXX       := /usr/bin/g++
 PKG       := paper_2110_10548_b200
 LIB       := $(PKG)/_lib
 INC       := -Iinclude -Ithird_party/absl_lite -Ithird_party
 CXXFLAGS  := -std=c++20 -O2 -fPIC -Wall -Wextra -Wno-missing-field-initializers
 ARCH      := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS   := -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -Wall \
+NVFLAGS   := -ccbin /usr/bin/g++ -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -Wall \
              --expt-relaxed-constexpr -Xptxas -v
 CUDA_INC  := -I/usr/local/cuda/include
 
@@ -51,7 +51,7 @@ $(LIB)/obj/cu_%.o: $(PKG)/csrc/exec/%.cu $(EXEC_HDRS)
 	$(NVCC) $(NVFLAGS) $(INC) -c $< -o $@ 2> $(LIB)/obj/cu_$*.ptxas.txt || (cat $(LIB)/obj/cu_$*.ptxas.txt; false)
 
 $(LIB)/libredsynth_b200.so: $(EXEC_OBJS) $(PLANNER_OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $^ -Xcompiler -pthread -lcuda
+	$(NVCC) -ccbin /usr/bin/g++ $(ARCH) -shared -o $@ $^ -Xcompiler -pthread -lcuda
 
 oracle:
 	$(MAKE) -C oracle numeric ref

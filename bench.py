@@ -1,0 +1,427 @@
+#!/usr/bin/env python
+"""redsynth-b200 bench — BASELINE.json config 2 on B200.
+
+Workload ("step"): execute EVERY synthesized program of config 2 once — all
+placements of axes [2,4] on the [(node,1),(socket,2),(GPU,4)] descriptor,
+reduce over axis 1 (254 programs) and over both axes (500 programs) — on
+K = 8 program devices ("slots") holding 256 MiB of bf16 each (synthetic
+N(0,1) data, rounded to bf16). With N GPUs the 8 slots are block-distributed
+(N=1: all 8 slots in one GPU's HBM = "local reduction and copy"; N=8: one slot
+per GPU, every step over NVLink/NVSwitch). Total work is fixed as N grows
+("strong" scaling).
+
+value = aggregate bus bandwidth of the step = sum over programs of
+K * D * 2(n-1)/n (nccl-tests AllReduce bus bytes, n = reduction-group size,
+D = 256 MiB) divided by the device-timed step (max over ranks).
+e2e   = the same metric through the C-ABI from pinned HOST buffers (H2D
+copy-in + program + D2H copy-out inside the timed region) on a fixed
+8-program sample of the same set.
+
+Usage: python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+For N>1 launch under torchrun (one rank per GPU, NCCL process group).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = BASELINE_METRIC = "synthesized-program reduce time (µs) & speedup vs NCCL AllReduce; bus GB/s"
+K_SLOTS = 8
+D_BYTES = 256 << 20
+DTYPE = "bf16"
+ELEMS = D_BYTES // 2
+REQUESTS = [[1], [0, 1]]
+SYSTEM = os.path.join(ROOT, "configs", "b200_sock.json")
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+NVLINK_PEAK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); nominal 900
+
+
+def programs():
+    from paper_2110_10548_b200 import planner
+    out = []
+    for red in REQUESTS:
+        syn = planner.synthesize(SYSTEM, [2, 4], red, payload_bytes=D_BYTES)
+        for mi, pl in enumerate(syn.placements):
+            for pi, prog in enumerate(pl.programs):
+                n = len(pl.partition[0])
+                out.append({"request": red, "matrix": mi, "index": pi, "prog": prog, "group_size": n,
+                            "factors": pl.factors})
+    return out
+
+
+def bus_bytes(entry):
+    n = entry["group_size"]
+    return K_SLOTS * D_BYTES * 2.0 * (n - 1) / n
+
+
+def algorithmic_link_bytes(prog, K, D):
+    """per step, max over groups of f(op, n) * c_g with
+    c_g = D * rows_g / K, rows_g = max non-empty rows over the members before
+    or after the step (simulator.cc:156-182); f = 2(n-1)/n AllReduce,
+    (n-1)/n ReduceScatter/AllGather, 1 Reduce/Broadcast."""
+    import numpy as np
+    from paper_2110_10548_b200 import planner
+    f = {0: lambda n: 2 * (n - 1) / n, 1: lambda n: (n - 1) / n, 2: lambda n: (n - 1) / n,
+         3: lambda n: 1.0, 4: lambda n: 1.0}
+    total = 0.0
+    prev = np.ones((K, K), dtype=bool)
+    for s, (op, groups) in enumerate(prog.steps):
+        post = planner.run_lowered(planner.LoweredProgram(steps=prog.steps[:s + 1]), K).any(axis=2)
+        worst = 0.0
+        for g in groups:
+            rows = max(max(int(prev[d].sum()) for d in g), max(int(post[d].sum()) for d in g))
+            worst = max(worst, f[op](len(g)) * D * rows / K)
+        total += worst
+        prev = post
+    return total
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.device_index = device_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.device_index), "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._pump, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU path for this workload = the C
+    numeric oracle (a restatement of semantics.cc:259-310; the reference's
+    own RunLowered is symbolic and moves no data), all host threads, one
+    full-size config-2 program per step from a fixed sample."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle import numeric, ref
+    progs = programs()
+    sample = [progs[i] for i in range(0, len(progs), max(1, len(progs) // 8))][:8]
+    threads = numeric.hardware_threads()
+    inputs = numeric.synthetic_inputs(K_SLOTS, ELEMS, numeric.BF16)
+    times, bytes_ = [], []
+    for it in range(args.warmup + args.steps):
+        e = sample[it % len(sample)]
+        bufs = [x.copy() for x in inputs]
+        t0 = time.perf_counter()
+        numeric.execute(e["prog"], K_SLOTS, bufs, numeric.BF16, nthreads=threads)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+            bytes_.append(bus_bytes(e))
+    value = sum(bytes_) / sum(times) / 1e9
+    symbolic_us = None
+    if ref.available():
+        symbolic_us = statistics.mean(ref.time_run_lowered(e["prog"].steps, K_SLOTS, 2000) for e in sample)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * sum(times) / len(times), 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "config 2 sample: one full-size program (8 slots x 256 MiB bf16) per step",
+                   "programs_in_sample": len(sample)},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": f"{len(sample)} config-2 programs at full size, one per step"},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_runlowered_us_per_program": symbolic_us,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--programs-out", default=None, help="write per-program device times (JSON)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2110_10548_b200 import executor
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    multi = world > 1
+    if multi:
+        dist.init_process_group("nccl", device_id=dev)
+    slot_rank = [d * world // K_SLOTS for d in range(K_SLOTS)]
+    if multi:
+        ctx = executor.Context.from_process_group(K_SLOTS, slot_rank, D_BYTES)
+    else:
+        ctx = executor.Context.local(K_SLOTS, [local_rank] * K_SLOTS, D_BYTES)
+
+    entries = programs()
+    # synthetic inputs for the slots this rank hosts (seed 1000+d)
+    gen = torch.Generator(device=dev)
+    for d in ctx.hosted_slots:
+        gen.manual_seed(1000 + d)
+        x = torch.randn(ELEMS, generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
+        ctx.buffer(d, ELEMS, "bf16").copy_(x)
+        del x
+    torch.cuda.synchronize()
+    plans = [ctx.compile(e["prog"], ELEMS, DTYPE) for e in entries]
+    launches_per_step = sum(p.launches for p in plans)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if multi:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step():
+        for p in plans:
+            p.run()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    ctx.synchronize()
+
+    # per-program device times (one pass, outside the timed region)
+    prog_us = []
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in plans]
+    for p, (a, b) in zip(plans, ev):
+        if multi:
+            dist.barrier()
+        a.record(stream)
+        p.run()
+        b.record(stream)
+    barrier()
+    prog_us = [a.elapsed_time(b) * 1e3 for a, b in ev]
+
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    barrier()
+    clocks = sampler.stop() if sampler else None
+    ctx.synchronize()
+    ms_local = t0.elapsed_time(t1)
+    if multi:
+        t = torch.tensor([ms_local], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+        pu = torch.tensor(prog_us, device=dev, dtype=torch.float64)
+        dist.all_reduce(pu, op=dist.ReduceOp.MAX)
+        prog_us = pu.tolist()
+    else:
+        ms_total = ms_local
+    ms_per_step = ms_total / args.steps
+    bus_per_step = sum(bus_bytes(e) for e in entries)
+    value = bus_per_step / (ms_per_step * 1e-3) / 1e9
+
+    # roofline of the dominant (only) kernel: the step kernel
+    if world == 1:
+        alg = 0.0
+        for p in plans:
+            for s in range(p.program.num_steps):
+                alg += p.step_bytes(s)[1]  # local mode: minimal HBM bytes of the tasks
+        peak, peak_kind = load_peaks()
+        achieved = alg / (ms_per_step * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": None,
+                    "note": f"algorithmic bytes = sum over tasks of (sources + destinations) x range "
+                            f"(minimal HBM traffic), per step {alg / 1e9:.2f} GB; peak {peak_kind}"}
+    else:
+        if world == K_SLOTS:
+            alg = sum(algorithmic_link_bytes(e["prog"], K_SLOTS, D_BYTES) for e in entries)
+        else:  # several slots per GPU: the plan's own per-GPU link bytes
+            alg = sum(p.step_bytes(s)[0] for p in plans for s in range(p.program.num_steps))
+        achieved = alg / (ms_per_step * 1e-3) / 1e9
+        roofline = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
+                    "frac": round(achieved / NVLINK_PEAK_GBS, 4), "traffic": None,
+                    "note": "per-GPU per-direction link bytes of SURVEY §8(d) (T_roof = sum_s max_g f*c_g) "
+                            "over the measured step; peak = measured peer copy 770 GB/s (900 nominal)"}
+
+    # per (request, placement): baseline AllReduce and best synthesized program
+    instances = {}
+    for e, us in zip(entries, prog_us):
+        key = (tuple(e["request"]), e["matrix"])
+        inst = instances.setdefault(key, {"request": e["request"], "factors": e["factors"], "best_us": 1e30,
+                                          "best": None, "allreduce_us": None, "programs": 0})
+        inst["programs"] += 1
+        if e["index"] == 0:
+            inst["allreduce_us"] = round(us, 2)
+        if us < inst["best_us"]:
+            inst["best_us"], inst["best"] = round(us, 2), e["prog"].text
+    inst_list = list(instances.values())
+
+    # end to end from pinned host memory (fixed sample)
+    e2e = None
+    if not args.no_e2e:
+        sample_idx = list(range(0, len(plans), max(1, len(plans) // 8)))[:8]
+        host = {}
+        for d in ctx.hosted_slots:
+            host[d] = ctx.buffer(d, ELEMS, "bf16").cpu().pin_memory()
+        hb = [host.get(d) for d in range(K_SLOTS)]
+        barrier()
+        h0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in sample_idx:
+            plans[i].run_host(hb)
+        e1.record(stream)
+        barrier()
+        e2e_ms = e0.elapsed_time(e1)
+        if multi:
+            t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        wall_ms = (time.perf_counter() - h0) * 1e3
+        nbytes = len(ctx.hosted_slots) * D_BYTES * len(sample_idx)
+        e2e = {"value": round(sum(bus_bytes(entries[i]) for i in sample_idx) / (e2e_ms * 1e-3) / 1e9, 3),
+               "unit": "GB/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "sample": f"{len(sample_idx)} programs (every {max(1, len(plans) // 8)}th), host buffers pinned",
+               "ms": round(e2e_ms, 2), "wall_ms": round(wall_ms, 2)}
+        del host, hb
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(entries)
+
+    if args.programs_out and rank == 0:
+        with open(args.programs_out, "w") as f:
+            json.dump([{"request": e["request"], "matrix": e["matrix"], "index": e["index"], "text": e["prog"].text,
+                        "sim_seconds": e["prog"].seconds, "measured_us": us} for e, us in zip(entries, prog_us)], f)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "config 2: all 754 synthesized programs (axes [2,4] on b200_sock, reduce {1} "
+                                   "and {0,1}), 8 slots x 256 MiB bf16",
+                       "slots_per_gpu": K_SLOTS // world, "programs": len(entries),
+                       "parallelism": f"{world} GPU(s), slots block-distributed",
+                       "l2": "inputs larger than L2 (8 x 256 MiB)"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+            "program_us": {"mean": round(statistics.mean(prog_us), 2), "min": round(min(prog_us), 2),
+                           "max": round(max(prog_us), 2)},
+            "instances": inst_list,
+        }
+        print(json.dumps(line), flush=True)
+    barrier()
+    for p in plans:
+        p.close()
+    if multi:
+        dist.barrier()
+    ctx.close()
+    if multi:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(entries):
+    """The C oracle on this host's cores over a bounded sample (2 programs
+    of config 2 at full size), reported beside the GPU number."""
+    try:
+        from oracle import numeric
+    except Exception as exc:  # pragma: no cover
+        return {"value": None, "unavailable": str(exc)}
+    threads = numeric.hardware_threads()
+    inputs = numeric.synthetic_inputs(K_SLOTS, ELEMS, numeric.BF16)
+    sample = [entries[0], entries[len(entries) // 2]]
+    t = 0.0
+    b = 0.0
+    for e in sample:
+        bufs = [x.copy() for x in inputs]
+        t0 = time.perf_counter()
+        numeric.execute(e["prog"], K_SLOTS, bufs, numeric.BF16, nthreads=threads)
+        t += time.perf_counter() - t0
+        b += bus_bytes(e)
+    return {"value": round(b / t / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+            "sample": f"{len(sample)} config-2 programs at full size (8 x 256 MiB bf16): "
+                      f"{sample[0]['prog'].text!r}, {sample[1]['prog'].text!r}",
+            "seconds": round(t, 2)}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,158 @@
+/* redsynth-b200 executor C-ABI — the drop-in boundary of the hot path.
+ *
+ * Executes a synthesized reduction program (a LoweredProgram: steps of
+ * AllReduce / ReduceScatter / AllGather / Reduce / Broadcast over disjoint
+ * device groups) on B200 GPUs with hand-written sm_100a peer-to-peer kernels.
+ * It is the data-moving sibling of the reference's symbolic executor
+ *
+ *   absl::StatusOr<StateContext> RunLowered(const LoweredProgram&, int k,
+ *                                           StepFailure* = nullptr);
+ *     — /root/reference/proj/include/redsynth/dsl.h:108, src/dsl.cc:142-164
+ *
+ * and is called by the C++ wrapper redsynth::Execute (redsynth/executor.h),
+ * by the Python host mirror (paper_2110_10548_b200/executor.py, ctypes) and by
+ * the bench. No torch or C++ types cross this boundary.
+ *
+ * Vocabulary. K "slots" = the K physical device ids of the program
+ * (SystemModel::device_count()). Slot d holds an N-element buffer; row r of it
+ * is elements [floor(r*N/K), floor((r+1)*N/K)). Slots live on "ranks" = GPUs.
+ * One process may drive all ranks (rs_ctx_create) or one rank each
+ * (rs_ctx_create_rank + IPC handle exchange, e.g. over torch.distributed).
+ * Several slots may share one GPU (e.g. K = 8 slots on 1 GPU = "local mode":
+ * every collective becomes an HBM-local sum/copy).
+ *
+ * Status codes mirror absl::StatusCode: 0 OK, 3 INVALID_ARGUMENT,
+ * 9 FAILED_PRECONDITION (a rule violation, same wording as
+ * StepFailure::Describe, dsl.cc:135-140), 13 INTERNAL (CUDA error or a
+ * device-side barrier timeout), 14 UNAVAILABLE (no GPU / extension missing).
+ * rs_last_error() returns the message of the last failing call on the thread.
+ */
+#ifndef REDSYNTH_EXEC_H_
+#define REDSYNTH_EXEC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rs_ctx rs_ctx;
+typedef struct rs_plan rs_plan;
+
+enum { RS_OK = 0, RS_INVALID_ARGUMENT = 3, RS_FAILED_PRECONDITION = 9, RS_INTERNAL = 13,
+       RS_UNAVAILABLE = 14 };
+/* Element types. */
+enum { RS_F32 = 0, RS_BF16 = 1, RS_I32 = 2 };
+/* Collective enum order of /root/reference/proj/include/redsynth/semantics.h:29-35. */
+enum { RS_OP_ALLREDUCE = 0, RS_OP_REDUCESCATTER = 1, RS_OP_ALLGATHER = 2, RS_OP_REDUCE = 3,
+       RS_OP_BROADCAST = 4 };
+
+#define RS_MAX_RANKS 8
+#define RS_IPC_HANDLE_BYTES 64
+
+/* Last error message of the calling thread ("" when none). */
+const char* rs_last_error(void);
+/* Library version string. */
+const char* rs_version(void);
+
+/* ---- contexts ----------------------------------------------------------- */
+
+/* Single process drives all K slots. cuda_ordinals[d] = GPU of slot d (the
+ * physical-device -> CUDA-ordinal map); repeated ordinals put several slots on
+ * one GPU. Each distinct ordinal is one rank. Allocates, per rank, a heap with
+ * one max_bytes buffer per hosted slot plus barrier flags, and enables peer
+ * access between the ranks. */
+int rs_ctx_create(int K, const int* cuda_ordinals, size_t max_bytes, rs_ctx** out);
+
+/* One process per GPU. slot_rank[d] = rank hosting slot d (0..world_size-1);
+ * this process is `rank` on GPU `cuda_ordinal`. Follow with
+ * rs_ctx_ipc_handle on every rank, an all-gather of the handles, and
+ * rs_ctx_open_peers. Every rank must then compile and run the same plans in
+ * the same order (like NCCL collectives). */
+int rs_ctx_create_rank(int K, const int* slot_rank, int world_size, int rank, int cuda_ordinal,
+                       size_t max_bytes, rs_ctx** out);
+/* Writes RS_IPC_HANDLE_BYTES bytes identifying this rank's heap. */
+int rs_ctx_ipc_handle(rs_ctx* ctx, void* out);
+/* handles = world_size * RS_IPC_HANDLE_BYTES bytes, rank-major. */
+int rs_ctx_open_peers(rs_ctx* ctx, const void* handles);
+
+/* Planning-only context: no GPU, no memory. Plans compiled on it can be
+ * inspected with rs_plan_describe_json but not run (CPU tests, tooling). */
+int rs_ctx_create_virtual(int K, const int* slot_rank, int world_size, rs_ctx** out);
+
+int rs_ctx_destroy(rs_ctx* ctx);
+
+/* Device pointer of the executor-owned buffer of slot d (slots hosted by this
+ * process only). Programs run in place on these buffers when rs_plan_run is
+ * given no user buffers. */
+int rs_ctx_buffer(rs_ctx* ctx, int slot, void** device_ptr);
+/* Number of ranks driven by this process and their CUDA ordinals. */
+int rs_ctx_local_ranks(rs_ctx* ctx, int* count, int* ordinals /* RS_MAX_RANKS */);
+/* Blocks until all work enqueued by this context is done; reports a
+ * device-side barrier timeout (INTERNAL) if one happened. */
+int rs_ctx_synchronize(rs_ctx* ctx);
+
+/* ---- plans -------------------------------------------------------------- */
+
+/* Compiles a lowered program (CSR: step_op[num_steps], step_group_ptr
+ * [num_steps+1] into group_member_ptr[num_groups+1] into members[]) for
+ * buffers of elems_per_device elements of `dtype`. Refuses programs that
+ * RunLowered refuses (same step index and violation), steps whose groups are
+ * not disjoint, and sizes above the context's max_bytes. */
+int rs_plan_compile(rs_ctx* ctx, int num_steps, const int32_t* step_op,
+                    const int32_t* step_group_ptr, const int32_t* group_member_ptr,
+                    const int32_t* members, size_t elems_per_device, int dtype, rs_plan** out);
+
+/* Enqueues the program (async). device_bufs: NULL = run in place on the
+ * context buffers; else K device pointers indexed by slot (entries of slots
+ * not hosted here are ignored) that are copied in before and out after.
+ * streams: NULL = the context's own streams; else one cudaStream_t per local
+ * rank, in rs_ctx_local_ranks order. */
+int rs_plan_run(rs_plan* plan, void* const* device_bufs, void* const* streams);
+
+/* End-to-end variant: host_bufs = K host pointers (pinned for speed) indexed
+ * by slot; copies each hosted slot's host buffer in (H2D), runs, copies the
+ * result back (D2H). Async on the given/own streams. */
+int rs_plan_run_host(rs_plan* plan, void* const* host_bufs, void* const* streams);
+
+/* Kernel launches one rs_plan_run performs (all local ranks). */
+int rs_plan_launch_count(rs_plan* plan, int* launches);
+
+/* Per-step summary, for reporting: algorithmic bytes each rank moves over
+ * links (link_bytes) and through HBM (hbm_bytes) in step s, maxed over ranks. */
+int rs_plan_step_bytes(rs_plan* plan, int step, double* link_bytes, double* hbm_bytes);
+
+/* Tuning knobs (0 = default): CTAs per launch cap and threads per CTA. */
+int rs_plan_set_launch(rs_plan* plan, int max_ctas, int threads);
+
+/* JSON dump of the compiled plan: per step, per rank, the entry-barrier
+ * ranks and tasks {lo, hi (bytes), vec, src slots, dst slots}. */
+int rs_plan_describe_json(rs_plan* plan, char** out_json);
+
+int rs_plan_destroy(rs_plan* plan);
+
+/* ---- planner (host C++ behind C, for the Python mirror) ------------------ */
+
+/* Runs EnumerateMatrices + Synthesize (+ Simulate for `seconds`) and returns
+ * JSON {"device_count", "matrices": [{"factors", "partition", "hierarchy",
+ * "programs": [{"text", "seconds", "steps": [{"op", "groups"}]}]}]}.
+ * Free with rs_free. */
+int rs_synthesize_json(const char* system_json, const int* axes, int n_axes,
+                       const int* reduce, int n_reduce, int size_limit, long long payload_bytes,
+                       int algo, char** out_json);
+/* RunPipeline + ReportToJson/ReportToCsv (byte-identical to the reference). */
+int rs_report(const char* system_path, const int* axes, int n_axes, const int* reduce,
+              int n_reduce, int size_limit, long long payload_bytes, int algo, int csv,
+              char** out);
+/* Symbolic RunLowered through the host planner (final state as K*K*K bytes). */
+int rs_run_lowered(int num_steps, const int32_t* step_op, const int32_t* step_group_ptr,
+                   const int32_t* group_member_ptr, const int32_t* members, int k,
+                   unsigned char* state, int* fail_step, int* fail_violation);
+void rs_free(char* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* REDSYNTH_EXEC_H_ */

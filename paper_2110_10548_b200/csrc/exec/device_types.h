@@ -1,0 +1,57 @@
+// Shared host/device launch records of the step kernel.
+#ifndef REDSYNTH_B200_EXEC_DEVICE_TYPES_H_
+#define REDSYNTH_B200_EXEC_DEVICE_TYPES_H_
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "redsynth_exec.h"
+
+namespace rs {
+
+// One contiguous byte range [lo, hi) (identical offsets in every slot buffer)
+// that one owner rank produces: dst_j[x] = src_0[x] + src_1[x] + ... for every
+// destination j (sum in source order; a single source is a raw copy).
+// Vector tasks are 16-byte aligned at both ends; scalar tasks are the < 16 B
+// heads/tails of unaligned ranges.
+struct Task {
+  uint64_t lo;
+  uint64_t hi;
+  uint32_t piece_begin;  // first piece of this task within its launch
+  uint32_t ptr_begin;    // srcs = ptrs[ptr_begin, +nsrc), dsts follow
+  uint16_t nsrc;
+  uint16_t ndst;
+  uint32_t vec;
+};
+
+// Everything one rank's kernel for one step needs (passed by value).
+struct StepArgs {
+  const Task* tasks;
+  void* const* ptrs;            // slot buffer bases as seen by this rank
+  uint32_t ntasks;
+  uint32_t npieces;
+  uint32_t piece_bytes;         // bytes per vector piece = threads * unroll * 16
+  int32_t dtype;
+  unsigned int* arrive_counter;  // this rank's CTA-arrival counter
+  int* error_flag;               // set to 1 on a barrier timeout
+  const uint64_t* inbox;         // this rank's flags, inbox[q] = last epoch of rank q
+  uint64_t* signal_ptrs[RS_MAX_RANKS];  // &inbox_of_rank_q[my_rank], every other rank q
+  uint32_t nsignal;
+  uint32_t nwait;
+  uint32_t nfinal;
+  uint32_t pad;
+  uint8_t wait_ranks[RS_MAX_RANKS];
+  uint8_t final_ranks[RS_MAX_RANKS];
+  uint64_t start_value;   // != 0: first step, publish "inputs ready" first
+  uint64_t wait_value;    // wait until inbox[q] >= wait_value for q in wait_ranks
+  uint64_t signal_value;  // published once every CTA finished its pieces
+  uint64_t final_value;   // last step: then wait for final_ranks to reach it
+  uint64_t timeout_ns;
+};
+
+cudaError_t LaunchStep(const StepArgs& args, int grid, int block, cudaStream_t stream);
+
+}  // namespace rs
+
+#endif  // REDSYNTH_B200_EXEC_DEVICE_TYPES_H_

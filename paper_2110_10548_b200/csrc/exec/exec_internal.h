@@ -1,0 +1,111 @@
+// Host-side executor objects behind the C-ABI (redsynth_exec.h).
+#ifndef REDSYNTH_B200_EXEC_INTERNAL_H_
+#define REDSYNTH_B200_EXEC_INTERNAL_H_
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "absl/status/status.h"
+#include "device_types.h"
+#include "redsynth_exec.h"
+
+namespace rs {
+
+// Heap layout of every rank (one cudaMalloc per rank, shared by IPC):
+//   [0, 64)        inbox: uint64 epoch per peer rank (written remotely)
+//   [256, 260)     CTA-arrival counter
+//   [512, 516)     barrier-timeout error flag
+//   [4096, ...)    one buffer per hosted slot, kSlotAlign-aligned stride
+constexpr size_t kInboxOffset = 0;
+constexpr size_t kCounterOffset = 256;
+constexpr size_t kErrorOffset = 512;
+constexpr size_t kDataOffset = 4096;
+constexpr size_t kSlotAlign = 1 << 21;  // 2 MiB: keeps every slot buffer 16 B (and page) aligned
+
+struct Rank {
+  int ordinal = -1;        // CUDA device (meaningful for ranks driven here)
+  bool driven = false;     // launched by this process
+  char* heap = nullptr;    // local device pointer (driven ranks)
+  size_t heap_bytes = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<char*> view;  // view[q] = rank q's heap as addressed from this rank
+  int max_ctas = 0;         // resident CTA capacity for the step kernel
+  int sm_count = 0;
+};
+
+class Context {
+ public:
+  int K = 0;
+  size_t max_bytes = 0;
+  size_t slot_stride = 0;
+  int world = 1;
+  int self_rank = -1;  // -1: single process drives every rank
+  bool peers_open = false;
+  bool is_virtual = false;  // planning only: no CUDA resources (CPU tests)
+  std::vector<int> slot_rank;      // slot -> rank
+  std::vector<int> slot_position;  // slot -> index among its rank's slots
+  std::vector<Rank> ranks;
+  uint64_t epoch = 1;              // next run's base epoch (identical on all ranks)
+  uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
+
+  size_t SlotOffset(int slot) const { return kDataOffset + slot_position[slot] * slot_stride; }
+  char* SlotPtr(int viewer, int slot) const {
+    return ranks[viewer].view[slot_rank[slot]] + SlotOffset(slot);
+  }
+  std::vector<int> DrivenRanks() const;
+};
+
+struct RankStep {
+  std::vector<Task> tasks;
+  std::vector<int> ptr_slots;  // slot id per pointer-table entry
+  uint32_t npieces = 0;
+  std::vector<uint8_t> wait;   // ranks to wait for before the step
+  double tx_bytes = 0, rx_bytes = 0, hbm_bytes = 0;
+};
+
+class Plan {
+ public:
+  Context* ctx = nullptr;
+  int num_steps = 0;
+  int dtype = 0;
+  size_t elems = 0;
+  size_t bytes = 0;  // per slot
+  int threads = 512;
+  int max_ctas = 0;  // 0 = resident capacity
+  std::vector<std::vector<RankStep>> steps;  // [step][rank]
+  std::vector<uint8_t> final_wait_bits;      // per rank: bitmask of ranks for the tail wait
+  // Device copies (per driven rank): all tasks / pointer tables of all steps.
+  std::vector<Task*> d_tasks;
+  std::vector<void**> d_ptrs;
+  std::vector<std::vector<size_t>> task_offset, ptr_offset;  // [rank][step]
+
+  ~Plan();
+};
+
+absl::Status CreateContext(int K, const int* ordinals, size_t max_bytes, Context** out);
+absl::Status CreateRankContext(int K, const int* slot_rank, int world, int rank, int ordinal,
+                               size_t max_bytes, Context** out);
+absl::Status CreateVirtualContext(int K, const int* slot_rank, int world, Context** out);
+absl::Status IpcHandle(Context* ctx, void* out);
+absl::Status OpenPeers(Context* ctx, const void* handles);
+absl::Status DestroyContext(Context* ctx);
+absl::Status Synchronize(Context* ctx);
+
+absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
+                         const int32_t* step_group_ptr, const int32_t* group_member_ptr,
+                         const int32_t* members, size_t elems, int dtype, Plan** out);
+absl::Status RunPlan(Plan* plan, void* const* device_bufs, void* const* host_bufs,
+                     void* const* streams);
+
+std::string DescribePlan(const Plan& plan);
+
+int MaxResidentCtas(int dtype, int threads);  // per SM, from the occupancy API
+
+absl::Status CudaStatus(cudaError_t err, const char* what);
+
+}  // namespace rs
+
+#endif  // REDSYNTH_B200_EXEC_INTERNAL_H_

@@ -1,0 +1,283 @@
+// The sm_100a step kernel: one launch per (program step, rank).
+//
+// A step of a lowered program is compiled (plan.cc) into "tasks": byte
+// ranges that one owner produces by summing its sources in group order and
+// storing the result to every destination. Sources and destinations are
+// slot buffers on this GPU or on NVSwitch peers (mapped peer pointers), so a
+// single pass covers every collective of /root/reference/proj/src/
+// semantics.cc:259-310:
+//   AllReduce      owner m: its 1/n slice of R, sources = all members,
+//                  destinations = all members (reduce-scatter + all-gather
+//                  fused into one pull-sum-push pass, 2(n-1)/n per link)
+//   ReduceScatter  owner m: run m of R, pull-sum into its own buffer
+//   Reduce         owners = non-roots, slices of R, sum -> root only
+//   AllGather /    owners = the receivers, each pulls a slice of a row from
+//   Broadcast      its holder and fans it out to the other receivers
+// Memory: 16-byte vector loads (ld.global.nc.L1::no_allocate) and stores,
+// 4 vectors in flight per thread per source, coalesced 512 B per warp.
+// Inter-GPU ordering: epoch flags (st.release.sys / ld.acquire.sys) in each
+// rank's heap; no NCCL, no host synchronisation between steps.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "device_types.h"
+
+namespace rs {
+namespace {
+
+constexpr int kUnroll = 4;
+
+__device__ __forceinline__ uint4 LoadStream(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void Store(void* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ uint64_t LoadAcquireSys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void StoreReleaseSys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void FenceSys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
+__device__ __forceinline__ uint64_t GlobalTimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Spin until *flag >= target; on timeout raise the error flag and give up
+// (the data is then wrong, but the GPU is not hung; the host reports it).
+__device__ void WaitAtLeast(const uint64_t* flag, uint64_t target, uint64_t timeout_ns,
+                            int* error_flag) {
+  if (LoadAcquireSys(flag) >= target) return;
+  const uint64_t t0 = GlobalTimer();
+  while (LoadAcquireSys(flag) < target) {
+    if (GlobalTimer() - t0 > timeout_ns) {
+      atomicExch(error_flag, 1);
+      return;
+    }
+    __nanosleep(32);
+  }
+}
+
+// ---- element arithmetic -----------------------------------------------
+
+// f32: IEEE adds in source order (no FMA possible: adds only).
+struct F32Acc {
+  float v[4];
+  __device__ __forceinline__ void Init(const uint4& r) {
+    v[0] = __uint_as_float(r.x); v[1] = __uint_as_float(r.y);
+    v[2] = __uint_as_float(r.z); v[3] = __uint_as_float(r.w);
+  }
+  __device__ __forceinline__ void Add(const uint4& r) {
+    v[0] = __fadd_rn(v[0], __uint_as_float(r.x)); v[1] = __fadd_rn(v[1], __uint_as_float(r.y));
+    v[2] = __fadd_rn(v[2], __uint_as_float(r.z)); v[3] = __fadd_rn(v[3], __uint_as_float(r.w));
+  }
+  __device__ __forceinline__ uint4 Pack() const {
+    return make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]),
+                      __float_as_uint(v[3]));
+  }
+};
+
+// bf16: widen to f32, add in source order, round to nearest even once.
+struct BF16Acc {
+  float v[8];
+  __device__ __forceinline__ static void Widen(uint32_t w, float& lo, float& hi) {
+    lo = __uint_as_float(w << 16);
+    hi = __uint_as_float(w & 0xffff0000u);
+  }
+  __device__ __forceinline__ void Init(const uint4& r) {
+    Widen(r.x, v[0], v[1]); Widen(r.y, v[2], v[3]); Widen(r.z, v[4], v[5]); Widen(r.w, v[6], v[7]);
+  }
+  __device__ __forceinline__ void Add(const uint4& r) {
+    float t[8];
+    Widen(r.x, t[0], t[1]); Widen(r.y, t[2], t[3]); Widen(r.z, t[4], t[5]); Widen(r.w, t[6], t[7]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __fadd_rn(v[i], t[i]);
+  }
+  __device__ __forceinline__ static uint32_t Narrow(float lo, float hi) {
+    __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);  // cvt.rn.bf16x2.f32
+    return *reinterpret_cast<uint32_t*>(&p);
+  }
+  __device__ __forceinline__ uint4 Pack() const {
+    return make_uint4(Narrow(v[0], v[1]), Narrow(v[2], v[3]), Narrow(v[4], v[5]),
+                      Narrow(v[6], v[7]));
+  }
+};
+
+// i32: two's-complement wrapping adds.
+struct I32Acc {
+  uint32_t v[4];
+  __device__ __forceinline__ void Init(const uint4& r) { v[0] = r.x; v[1] = r.y; v[2] = r.z; v[3] = r.w; }
+  __device__ __forceinline__ void Add(const uint4& r) { v[0] += r.x; v[1] += r.y; v[2] += r.z; v[3] += r.w; }
+  __device__ __forceinline__ uint4 Pack() const { return make_uint4(v[0], v[1], v[2], v[3]); }
+};
+
+template <int DT> struct AccOf;
+template <> struct AccOf<RS_F32> { using T = F32Acc; };
+template <> struct AccOf<RS_BF16> { using T = BF16Acc; };
+template <> struct AccOf<RS_I32> { using T = I32Acc; };
+
+// One vector piece: bytes [begin, end) of the task, 16-byte aligned.
+template <int DT>
+__device__ __forceinline__ void VectorPiece(const Task& t, void* const* ptrs, uint64_t begin,
+                                            uint64_t end) {
+  using Acc = typename AccOf<DT>::T;
+  uint64_t off[kUnroll];
+  bool ok[kUnroll];
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {
+    off[u] = begin + (static_cast<uint64_t>(u) * blockDim.x + threadIdx.x) * 16u;
+    ok[u] = off[u] < end;
+  }
+  void* const* src = ptrs + t.ptr_begin;
+  void* const* dst = src + t.nsrc;
+  uint4 raw[kUnroll] = {};
+  const char* s0 = static_cast<const char*>(src[0]);
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u)
+    if (ok[u]) raw[u] = LoadStream(s0 + off[u]);
+  if (t.nsrc > 1) {
+    Acc acc[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) acc[u].Init(raw[u]);
+    for (int i = 1; i < t.nsrc; ++i) {
+      const char* si = static_cast<const char*>(src[i]);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+        if (ok[u]) raw[u] = LoadStream(si + off[u]);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) acc[u].Add(raw[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) raw[u] = acc[u].Pack();
+  }
+  for (int j = 0; j < t.ndst; ++j) {
+    char* d = static_cast<char*>(dst[j]);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (ok[u]) Store(d + off[u], raw[u]);
+  }
+}
+
+// A scalar task (< 16 bytes): one element per thread.
+template <int DT>
+__device__ void ScalarTask(const Task& t, void* const* ptrs) {
+  constexpr int kEs = DT == RS_BF16 ? 2 : 4;
+  const uint64_t x = t.lo + static_cast<uint64_t>(threadIdx.x) * kEs;
+  if (x >= t.hi) return;
+  void* const* src = ptrs + t.ptr_begin;
+  void* const* dst = src + t.nsrc;
+  if (DT == RS_BF16) {
+    const uint16_t first = *reinterpret_cast<const uint16_t*>(static_cast<const char*>(src[0]) + x);
+    uint16_t out = first;
+    if (t.nsrc > 1) {
+      float acc = __uint_as_float(static_cast<uint32_t>(first) << 16);
+      for (int i = 1; i < t.nsrc; ++i) {
+        const uint16_t h = *reinterpret_cast<const uint16_t*>(static_cast<const char*>(src[i]) + x);
+        acc = __fadd_rn(acc, __uint_as_float(static_cast<uint32_t>(h) << 16));
+      }
+      __nv_bfloat16 b = __float2bfloat16_rn(acc);
+      out = *reinterpret_cast<uint16_t*>(&b);
+    }
+    for (int j = 0; j < t.ndst; ++j) *reinterpret_cast<uint16_t*>(static_cast<char*>(dst[j]) + x) = out;
+  } else {
+    uint32_t out = *reinterpret_cast<const uint32_t*>(static_cast<const char*>(src[0]) + x);
+    for (int i = 1; i < t.nsrc; ++i) {
+      const uint32_t w = *reinterpret_cast<const uint32_t*>(static_cast<const char*>(src[i]) + x);
+      if (DT == RS_F32) out = __float_as_uint(__fadd_rn(__uint_as_float(out), __uint_as_float(w)));
+      else out += w;
+    }
+    for (int j = 0; j < t.ndst; ++j) *reinterpret_cast<uint32_t*>(static_cast<char*>(dst[j]) + x) = out;
+  }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(1024) StepKernel(const __grid_constant__ StepArgs a) {
+  // 1. First step of a run: publish "my inputs are in place" to every peer.
+  if (a.start_value != 0 && blockIdx.x == 0 && threadIdx.x < a.nsignal) {
+    FenceSys();
+    StoreReleaseSys(a.signal_ptrs[threadIdx.x], a.start_value);
+  }
+  // 2. Entry barrier: the ranks whose buffers this step touches (and whose
+  //    previous-step writers) have finished the previous step.
+  if (threadIdx.x < a.nwait) {
+    WaitAtLeast(a.inbox + a.wait_ranks[threadIdx.x], a.wait_value, a.timeout_ns, a.error_flag);
+  }
+  __syncthreads();
+
+  // 3. Pieces, grid-strided; tasks are ordered by piece_begin.
+  uint32_t cur = 0;
+  for (uint32_t p = blockIdx.x; p < a.npieces; p += gridDim.x) {
+    while (cur + 1 < a.ntasks && a.tasks[cur + 1].piece_begin <= p) ++cur;
+    const Task& t = a.tasks[cur];
+    if (t.vec) {
+      const uint64_t begin = t.lo + static_cast<uint64_t>(p - t.piece_begin) * a.piece_bytes;
+      const uint64_t end = min(t.hi, begin + a.piece_bytes);
+      VectorPiece<DT>(t, a.ptrs, begin, end);
+    } else {
+      ScalarTask<DT>(t, a.ptrs);
+    }
+  }
+
+  // 4. Exit: the last CTA to finish publishes the step's epoch to all ranks.
+  if (a.nsignal == 0 && a.nfinal == 0) return;
+  FenceSys();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(a.arrive_counter, 1u);
+    if (prev == gridDim.x - 1) {
+      atomicExch(a.arrive_counter, 0u);
+      FenceSys();
+      for (uint32_t q = 0; q < a.nsignal; ++q) StoreReleaseSys(a.signal_ptrs[q], a.signal_value);
+      // 5. Last step: the run is complete here only once every rank that
+      //    writes into our slots has finished too.
+      for (uint32_t i = 0; i < a.nfinal; ++i) {
+        WaitAtLeast(a.inbox + a.final_ranks[i], a.final_value, a.timeout_ns, a.error_flag);
+      }
+    }
+  }
+}
+
+}  // namespace
+
+int MaxResidentCtas(int dtype, int threads) {
+  int blocks = 0;
+  cudaError_t e = cudaSuccess;
+  switch (dtype) {
+    case RS_F32: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_F32>, threads, 0); break;
+    case RS_BF16: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_BF16>, threads, 0); break;
+    default: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_I32>, threads, 0); break;
+  }
+  if (e != cudaSuccess || blocks < 1) {
+    cudaGetLastError();
+    return 1;
+  }
+  return blocks;
+}
+
+cudaError_t LaunchStep(const StepArgs& args, int grid, int block, cudaStream_t stream) {
+  switch (args.dtype) {
+    case RS_F32: StepKernel<RS_F32><<<grid, block, 0, stream>>>(args); break;
+    case RS_BF16: StepKernel<RS_BF16><<<grid, block, 0, stream>>>(args); break;
+    case RS_I32: StepKernel<RS_I32><<<grid, block, 0, stream>>>(args); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace rs

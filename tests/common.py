@@ -1,0 +1,91 @@
+"""Shared helpers for the test-suite (loads golden program sets, builds the
+numpy plan simulator used by the CPU plan-compiler tests)."""
+import json
+import os
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+GOLDEN_SETS = ["cfg1", "cfg2_r1", "cfg2_r01", "cfg3_r0", "cfg3_r1", "cfg3_r2", "cfg3_r01", "cfg3_r02",
+               "cfg3_r12", "k2_flat", "k4_flat", "k4_sock", "k8_flat", "k8_sock", "a100_2node_r0"]
+
+
+def load_golden(name):
+    with open(os.path.join(GOLDEN, f"programs_{name}.json")) as f:
+        return json.load(f)
+
+
+def golden_programs(name):
+    """[(matrix index, program index, LoweredProgram, partition)]"""
+    from paper_2110_10548_b200.planner import LoweredProgram
+    doc = load_golden(name)
+    out = []
+    for mi, m in enumerate(doc["matrices"]):
+        for pi, p in enumerate(m["programs"]):
+            out.append((mi, pi, LoweredProgram.from_json(p), m["partition"]))
+    return doc["device_count"], out
+
+
+def bf16_round(x_f32):
+    import ml_dtypes
+    return x_f32.astype(ml_dtypes.bfloat16).view(np.uint16)
+
+
+def bf16_widen(u16):
+    return (u16.astype(np.uint32) << 16).view(np.float32)
+
+
+def simulate_plan(desc, bufs, dtype):
+    """Executes a compiled plan (Plan.describe()) over numpy slot buffers.
+
+    Every task of a step is checked for hazards first (a byte written by one
+    task may not be touched by another task of the same step), then executed:
+    dst_j = src_0 + src_1 + ... in source order (f32 adds / bf16 via f32 with
+    one RNE rounding / wrapping i32), a single source being a raw copy —
+    exactly the step kernel's contract. Returns nothing; bufs are updated."""
+    es = 2 if dtype == 1 else 4
+    view = {0: np.float32, 1: np.uint16, 2: np.int32}[dtype]
+    for step in desc["steps"]:
+        tasks = [t for r in step["ranks"] for t in r["tasks"]]
+        # hazard check: per slot, written intervals vs every other task's accesses
+        acc = {}
+        for i, t in enumerate(tasks):
+            for s in t["src"]:
+                acc.setdefault(s, []).append((t["lo"], t["hi"], i, "r"))
+            for d in t["dst"]:
+                acc.setdefault(d, []).append((t["lo"], t["hi"], i, "w"))
+        for slot, ivs in acc.items():
+            ivs.sort()
+            for a in range(len(ivs)):
+                for b in range(a + 1, len(ivs)):
+                    if ivs[b][0] >= ivs[a][1]:
+                        break
+                    if ivs[a][2] != ivs[b][2] and "w" in (ivs[a][3], ivs[b][3]):
+                        raise AssertionError(f"hazard on slot {slot}: {ivs[a]} vs {ivs[b]}")
+        for t in tasks:
+            assert t["lo"] % es == 0 and t["hi"] % es == 0
+            if t["vec"]:
+                assert t["lo"] % 16 == 0 and t["hi"] % 16 == 0
+            else:
+                assert t["hi"] - t["lo"] < 16
+            lo, hi = t["lo"] // es, t["hi"] // es
+            srcs = [bufs[s].view(view)[lo:hi] for s in t["src"]]
+            if len(srcs) == 1:
+                out = srcs[0].copy()
+            elif dtype == 0:
+                out = srcs[0].copy()
+                for x in srcs[1:]:
+                    out = (out + x).astype(np.float32)
+            elif dtype == 1:
+                accf = bf16_widen(srcs[0])
+                for x in srcs[1:]:
+                    accf = (accf + bf16_widen(x)).astype(np.float32)
+                out = bf16_round(accf)
+            else:
+                out = srcs[0].copy()
+                for x in srcs[1:]:
+                    out = (out + x).astype(np.int32)
+            for d in t["dst"]:
+                bufs[d].view(view)[lo:hi] = out

@@ -1,0 +1,78 @@
+"""One process per GPU (the bench's launch shape): CUDA-IPC heaps exchanged
+over torch.distributed, each rank enqueues only its own kernels, peers sync
+through epoch flags in each other's memory. Compared bit-exactly with the C
+oracle on every rank."""
+import os
+
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+    pytest.skip("needs >= 2 GPUs", allow_module_level=True)
+
+
+def _worker(rank, world, port, result_dir):
+    import sys
+    import traceback
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    ok = True
+    msg = ""
+    try:
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+        os.environ["RS_BARRIER_TIMEOUT_S"] = "10"
+        torch.cuda.set_device(rank)
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        from common import golden_programs
+        from oracle import numeric
+        from paper_2110_10548_b200 import executor
+        K = 8
+        slot_rank = [d * world // K for d in range(K)]
+        ctx = executor.Context.from_process_group(K, slot_rank, 32 << 20)
+        for name, N, dt, stride, runs in [("cfg2_r1", 3001, numeric.BF16, 5, 1),
+                                          ("cfg2_r01", 4097, numeric.F32, 7, 2),
+                                          ("cfg2_r01", 4 << 20, numeric.BF16, 100, 2)]:
+            _, progs = golden_programs(name)
+            inputs = numeric.synthetic_inputs(K, N, dt)
+            es = 2 if dt == numeric.BF16 else 4
+            for _, _, prog, _ in progs[::stride]:
+                for d in ctx.hosted_slots:
+                    ctx.write(d, inputs[d])
+                plan = ctx.compile(prog, N, dt)
+                for _ in range(runs):
+                    plan.run()
+                ctx.synchronize()
+                want = [x.copy() for x in inputs]
+                for _ in range(runs):
+                    numeric.execute(prog, K, want, dt)
+                for d in ctx.hosted_slots:
+                    if not np.array_equal(ctx.read(d, N * es), want[d].view(np.uint8)):
+                        raise AssertionError(f"rank {rank} slot {d} mismatch: {prog.text}")
+                plan.close()
+                dist.barrier()
+        dist.barrier()
+        ctx.close()
+        dist.destroy_process_group()
+    except Exception:
+        ok = False
+        msg = traceback.format_exc()
+    with open(os.path.join(result_dir, f"r{rank}.txt"), "w") as f:
+        f.write("OK" if ok else msg)
+
+
+@pytest.mark.parametrize("world", [2])
+def test_ipc_two_processes(tmp_path, world):
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.start_processes(_worker, args=(world, port, str(tmp_path)), nprocs=world, start_method="spawn", join=True)
+    for r in range(world):
+        text = (tmp_path / f"r{r}.txt").read_text()
+        assert text == "OK", text

@@ -1,0 +1,180 @@
+"""GPU parity: the sm_100a executor against the C oracle, through the C-ABI.
+
+Bit-exact for every dtype (the kernels sum members in the oracle's order and
+round bf16 once), on every synthesized program of configs 1-3, plus full-size
+BASELINE buffers, several slot->GPU mappings, repeated runs (epoch flags),
+the user-buffer and host-buffer paths and refusal behaviour.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from common import golden_programs
+from oracle import numeric
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2110_10548_b200 import executor  # noqa: E402
+from paper_2110_10548_b200._native import ExecError  # noqa: E402
+
+os.environ.setdefault("RS_BARRIER_TIMEOUT_S", "10")
+ES = {numeric.F32: 4, numeric.BF16: 2, numeric.I32: 4}
+NGPU = torch.cuda.device_count()
+
+
+def _run(ctx, prog, K, N, dtype, inputs=None, runs=1):
+    inputs = inputs if inputs is not None else numeric.synthetic_inputs(K, N, dtype)
+    for d in range(K):
+        ctx.write(d, inputs[d])
+    plan = ctx.compile(prog, N, dtype)
+    for _ in range(runs):
+        plan.run()
+    ctx.synchronize()
+    got = [ctx.read(d, N * ES[dtype]) for d in range(K)]
+    want = [x.copy() for x in inputs]
+    for _ in range(runs):
+        numeric.execute(prog, K, want, dtype)
+    for d in range(K):
+        assert np.array_equal(got[d], want[d].view(np.uint8)), (prog.text, d)
+    plan.close()
+
+
+@pytest.fixture(scope="module")
+def local8():
+    ctx = executor.Context.local(8, [0] * 8, max_bytes=256 << 20)
+    yield ctx
+    ctx.close()
+
+
+@pytest.mark.parametrize("dtype", [numeric.F32, numeric.BF16, numeric.I32])
+def test_config1_every_program_local(local8, dtype):
+    K, progs = golden_programs("cfg1")
+    for _, _, prog, _ in progs:
+        _run(local8, prog, K, 4099, dtype)
+
+
+def test_config1_full_size_f32_local(local8):
+    """Config 1 exactly: 64 MiB fp32 per device, all 8 synthesized programs."""
+    K, progs = golden_programs("cfg1")
+    N = 16 * 1024 * 1024
+    inputs = numeric.synthetic_inputs(K, N, numeric.F32)
+    for _, _, prog, _ in progs:
+        _run(local8, prog, K, N, numeric.F32, inputs=inputs)
+
+
+@pytest.mark.parametrize("name", ["cfg2_r1", "cfg2_r01"])
+def test_config2_every_program_bf16_local(local8, name):
+    K, progs = golden_programs(name)
+    for _, _, prog, _ in progs:
+        _run(local8, prog, K, 2053, numeric.BF16)
+
+
+def test_config2_full_size_bf16_local(local8):
+    """256 MiB bf16 per device (config 2's size) on a sample of programs."""
+    K, progs = golden_programs("cfg2_r01")
+    N = 128 * 1024 * 1024
+    inputs = numeric.synthetic_inputs(K, N, numeric.BF16)
+    for _, _, prog, _ in progs[::125]:
+        _run(local8, prog, K, N, numeric.BF16, inputs=inputs)
+
+
+@pytest.mark.parametrize("name", ["cfg3_r0", "cfg3_r1", "cfg3_r2", "cfg3_r01", "cfg3_r02", "cfg3_r12"])
+def test_config3_every_program_f32_local(local8, name):
+    K, progs = golden_programs(name)
+    for _, _, prog, _ in progs:
+        _run(local8, prog, K, 1001, numeric.F32)
+
+
+@pytest.mark.parametrize("N", [0, 1, 7, 8, 9, 33, 1023, 65537])
+def test_ragged_sizes_local(local8, N):
+    K, progs = golden_programs("cfg2_r01")
+    for _, _, prog, _ in progs[::40]:
+        for dt in (numeric.BF16, numeric.I32):
+            _run(local8, prog, K, N, dt)
+
+
+def test_repeated_runs_chain(local8):
+    K, progs = golden_programs("cfg2_r1")
+    for _, _, prog, _ in progs[::50]:
+        _run(local8, prog, K, 5000, numeric.I32, runs=3)
+
+
+def test_user_and_host_buffer_paths(local8):
+    K, progs = golden_programs("cfg2_r01")
+    N = 10007
+    prog = progs[123][2]
+    inputs = numeric.synthetic_inputs(K, N, numeric.F32)
+    want = [x.copy() for x in inputs]
+    numeric.execute(prog, K, want, numeric.F32)
+    plan = local8.compile(prog, N, "f32")
+    dev = [torch.from_numpy(x.copy()).cuda() for x in inputs]
+    plan.run(bufs=dev)
+    local8.synchronize()
+    for d in range(K):
+        assert np.array_equal(dev[d].cpu().numpy(), want[d])
+    host = [torch.from_numpy(x.copy()).pin_memory() for x in inputs]
+    plan.run_host(host)
+    local8.synchronize()
+    for d in range(K):
+        assert np.array_equal(host[d].numpy(), want[d])
+
+
+def test_refusal_launches_nothing(local8):
+    from paper_2110_10548_b200.planner import LoweredProgram
+    bad = LoweredProgram(steps=[(3, [[0, 1, 2, 3]]), (3, [[0, 1, 2, 3]])])
+    with pytest.raises(ExecError) as e:
+        local8.compile(bad, 100, "f32")
+    assert e.value.code == 9
+    assert e.value.message == "step 1: Reduce over devices {0,1,2,3}: devices hold different chunk sets"
+    K, progs = golden_programs("cfg1")  # the context still works afterwards
+    _run(local8, progs[0][2], K, 100, numeric.F32)
+
+
+def test_oversize_refused(local8):
+    K, progs = golden_programs("cfg1")
+    with pytest.raises(ExecError) as e:
+        local8.compile(progs[0][2], (256 << 20) // 4 + 1, "f32")
+    assert e.value.code == 3
+
+
+# ---- several GPUs, one process --------------------------------------------
+
+@pytest.mark.multigpu
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("mapping", ["block", "interleave"])
+def test_two_gpus_config2(mapping):
+    ords = [d * 2 // 8 for d in range(8)] if mapping == "block" else [d % 2 for d in range(8)]
+    ctx = executor.Context.local(8, ords, max_bytes=64 << 20)
+    try:
+        for name in ("cfg2_r1", "cfg2_r01"):
+            K, progs = golden_programs(name)
+            for _, _, prog, _ in progs[::3]:
+                _run(ctx, prog, K, 3001, numeric.BF16)
+        K, progs = golden_programs("cfg2_r01")
+        for _, _, prog, _ in progs[::100]:
+            _run(ctx, prog, K, 8 << 20, numeric.BF16, runs=2)
+    finally:
+        ctx.close()
+
+
+@pytest.mark.multigpu
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_one_slot_per_gpu_small_k():
+    n = min(NGPU, 8)
+    name = {2: "k2_flat", 4: "k4_sock", 8: "k8_sock"}.get(n)
+    if name is None:
+        pytest.skip("GPU count without a golden set")
+    ctx = executor.Context.local(n, list(range(n)), max_bytes=64 << 20)
+    try:
+        K, progs = golden_programs(name)
+        for _, _, prog, _ in progs:
+            _run(ctx, prog, K, 4097, numeric.F32)
+        for _, _, prog, _ in progs[:4]:
+            _run(ctx, prog, K, 16 << 20, numeric.BF16, runs=3)
+    finally:
+        ctx.close()

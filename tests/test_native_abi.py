@@ -1,0 +1,55 @@
+"""The C-ABI library loads on a CPU-only machine and exports every symbol
+include/redsynth_exec.h declares; calls that need a GPU fail with a status
+code instead of crashing. No compute is attempted here."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from common import ROOT
+from paper_2110_10548_b200 import _native as nat
+
+
+def _declared():
+    text = open(os.path.join(ROOT, "include", "redsynth_exec.h")).read()
+    return sorted(set(re.findall(r"\b(rs_[a-z_]+)\s*\(", text)))
+
+
+def test_header_and_binding_agree():
+    assert sorted(nat.EXPORTED_SYMBOLS) == _declared()
+
+
+def test_library_exports_every_declared_symbol():
+    lib = nat.lib()
+    for name in _declared():
+        assert hasattr(lib, name), name
+    assert b"sm_100a" in lib.rs_version()
+
+
+def test_sass_is_sm100a():
+    # the executor library carries an sm_100a cubin (cuobjdump lists the arch)
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([exe, "--list-elf", nat.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_create_without_gpu_reports_status():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    h = ctypes.c_void_p()
+    code = nat.lib().rs_ctx_create(2, nat.int_array([0, 0]), 1 << 20, ctypes.byref(h))
+    assert code in (nat.RS_UNAVAILABLE, nat.RS_INTERNAL, nat.RS_INVALID_ARGUMENT)
+    assert nat.lib().rs_last_error()
+
+
+def test_null_arguments_are_invalid():
+    lib = nat.lib()
+    assert lib.rs_ctx_create(2, None, 1 << 20, None) == nat.RS_INVALID_ARGUMENT
+    assert lib.rs_plan_run(None, None, None) == nat.RS_INVALID_ARGUMENT
+    assert lib.rs_ctx_destroy(None) == nat.RS_OK

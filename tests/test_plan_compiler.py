@@ -1,0 +1,182 @@
+"""The executor's plan compiler on CPU (planning-only contexts, no GPU).
+
+Every compiled plan is executed by a numpy simulator of the step kernel's
+contract (tests/common.py::simulate_plan), which first proves the step's
+tasks hazard-free (no byte written by one task is touched by another), and
+the result must equal the C oracle bit for bit — for every synthesized
+program of the baseline configs, several slot->GPU mappings, and ragged
+sizes. Barrier sets are checked against an independent derivation.
+"""
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+from common import GOLDEN, golden_programs, simulate_plan
+from oracle import numeric
+from paper_2110_10548_b200 import executor
+from paper_2110_10548_b200._native import ExecError
+
+MAPPINGS = {
+    "local": lambda K: ([0] * K, 1),
+    "two_gpus": lambda K: ([d * 2 // K for d in range(K)], 2),
+    "four_gpus": lambda K: ([d * 4 // K for d in range(K)], 4),
+    "one_per_gpu": lambda K: (list(range(K)), K),
+    "interleaved2": lambda K: ([d % 2 for d in range(K)], 2),
+}
+
+
+def _compile(prog, K, mapping, N, dtype):
+    slot_rank, world = MAPPINGS[mapping](K)
+    ctx = executor.Context.virtual(K, slot_rank, world)
+    plan = ctx.compile(prog, N, dtype)
+    return ctx, plan, plan.describe()
+
+
+def _check(prog, K, mapping, N, dtype):
+    ctx, plan, desc = _compile(prog, K, mapping, N, dtype)
+    inputs = numeric.synthetic_inputs(K, N, dtype)
+    want = [x.copy() for x in inputs]
+    numeric.execute(prog, K, want, dtype, nthreads=1)
+    got = [x.copy() for x in inputs]
+    simulate_plan(desc, got, dtype)
+    for d in range(K):
+        assert np.array_equal(got[d].view(np.uint8), want[d].view(np.uint8)), (prog.text, mapping, d)
+    return desc
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2_r1", "cfg2_r01"])
+def test_every_program_bit_exact_bf16_one_per_gpu(name):
+    K, progs = golden_programs(name)
+    for _, _, prog, _ in progs:
+        _check(prog, K, "one_per_gpu", 333, numeric.BF16)
+
+
+@pytest.mark.parametrize("name", ["cfg3_r0", "cfg3_r1", "cfg3_r2", "cfg3_r01", "cfg3_r02", "cfg3_r12"])
+def test_every_config3_program_bit_exact_f32(name):
+    K, progs = golden_programs(name)
+    for _, _, prog, _ in progs:
+        _check(prog, K, "one_per_gpu", 61, numeric.F32)
+
+
+@pytest.mark.parametrize("mapping", ["local", "two_gpus", "four_gpus", "interleaved2"])
+@pytest.mark.parametrize("dtype", [numeric.F32, numeric.BF16, numeric.I32])
+def test_sampled_programs_other_mappings(mapping, dtype):
+    rng = random.Random(7)
+    for name in ("cfg2_r01", "cfg2_r1", "cfg3_r12", "k8_sock"):
+        K, progs = golden_programs(name)
+        for _, _, prog, _ in rng.sample(progs, min(25, len(progs))):
+            _check(prog, K, mapping, rng.choice([8, 15, 64, 257, 1000, 4099]), dtype)
+
+
+@pytest.mark.parametrize("N", [0, 1, 5, 8, 9, 31, 127])
+def test_ragged_and_tiny_sizes(N):
+    K, progs = golden_programs("cfg2_r01")
+    for _, _, prog, _ in progs[::20]:
+        _check(prog, K, "one_per_gpu", N, numeric.BF16)
+        _check(prog, K, "local", N, numeric.I32)
+
+
+def test_small_k_sets():
+    for name in ("k2_flat", "k4_flat", "k4_sock", "k8_flat"):
+        K, progs = golden_programs(name)
+        for _, _, prog, _ in progs:
+            for mapping in ("local", "one_per_gpu"):
+                _check(prog, K, mapping, 1001, numeric.F32)
+
+
+def _group_of(prog, s, d):
+    if s < 0:
+        return [d]
+    for g in prog.steps[s][1]:
+        if d in g:
+            return g
+    return [d]
+
+
+def test_barrier_sets_match_independent_derivation():
+    K, progs = golden_programs("cfg2_r01")
+    for mapping in ("one_per_gpu", "two_gpus", "interleaved2"):
+        slot_rank, world = MAPPINGS[mapping](K)
+        for _, _, prog, _ in progs[::7]:
+            _, _, desc = _compile(prog, K, mapping, 100, numeric.F32)
+            for s, step in enumerate(desc["steps"]):
+                for r, rk in enumerate(step["ranks"]):
+                    expect = set()
+                    for d in range(K):
+                        if slot_rank[d] != r:
+                            continue
+                        for q in _group_of(prog, s, d):
+                            for p in _group_of(prog, s - 1, q):
+                                expect.add(slot_rank[p])
+                    expect.discard(r)
+                    assert set(rk["wait"]) == expect
+            for r in range(world):
+                expect = {slot_rank[p] for d in range(K) if slot_rank[d] == r
+                          for p in _group_of(prog, len(prog.steps) - 1, d)} - {r}
+                assert set(desc["final_wait"][r]) == expect
+
+
+def test_allreduce_is_one_pass_two_shot():
+    """Baseline AllReduce over n members: each owner reduces a 1/n slice
+    (16-byte aligned cut points) and pushes it to all n members."""
+    K, progs = golden_programs("cfg2_r01")
+    prog = progs[0][2]
+    assert prog.text == "Slice(root) InsideGroup AllReduce"
+    _, plan, desc = _compile(prog, K, "one_per_gpu", 1 << 20, numeric.BF16)
+    step = desc["steps"][0]
+    sizes = [sum(t["hi"] - t["lo"] for t in rk["tasks"]) for rk in step["ranks"]]
+    assert max(sizes) - min(sizes) <= 16
+    for rk in step["ranks"]:
+        for t in rk["tasks"]:
+            assert len(t["src"]) == 8 and len(t["dst"]) == 8
+    link, _ = plan.step_bytes(0)
+    D = (1 << 20) * 2
+    assert abs(link - 2 * 7 / 8 * D) <= 64  # 2(n-1)/n D per direction
+
+
+def test_broadcast_relay_balances_root_link():
+    """Reduce -> Broadcast over 8: the root sends each byte once (relay by
+    the receivers), so its per-direction traffic is ~1 x D, not 7 x D."""
+    K, progs = golden_programs("k8_flat")
+    prog = next(p for _, _, p, _ in progs if p.text.endswith("Reduce; Slice(root) InsideGroup Broadcast"))
+    _, plan, desc = _compile(prog, K, "one_per_gpu", 1 << 20, numeric.F32)
+    D = (1 << 20) * 4
+    for s in range(2):
+        link, _ = plan.step_bytes(s)
+        assert link <= 1.01 * D, (s, link / D)
+
+
+def test_refusals_match_reference():
+    from paper_2110_10548_b200.planner import LoweredProgram
+    cases = json.load(open(os.path.join(GOLDEN, "refusals.json")))
+    ctx = executor.Context.virtual(8, list(range(8)), 8)
+    for c in cases:
+        prog = LoweredProgram(steps=[(op, gs) for op, gs in c["steps"]])
+        if c["code"] == 0:
+            ctx.compile(prog, 64, "f32")
+            continue
+        with pytest.raises(ExecError) as e:
+            ctx.compile(prog, 64, "f32")
+        assert e.value.code == c["code"] and e.value.message == c["message"]
+
+
+def test_structural_refusals():
+    from paper_2110_10548_b200.planner import LoweredProgram
+    ctx = executor.Context.virtual(4, [0, 1, 2, 3], 4)
+    with pytest.raises(ExecError) as e:
+        ctx.compile(LoweredProgram(steps=[(0, [])]), 8)
+    assert e.value.code == 3 and e.value.message == "step 0 has no device groups"
+    with pytest.raises(ExecError) as e:  # out of range -> reference violation name
+        ctx.compile(LoweredProgram(steps=[(0, [[0, 9]])]), 8)
+    assert e.value.code == 9 and "device outside the state context" in e.value.message
+    with pytest.raises(ExecError) as e:  # groups not disjoint: executor precondition
+        ctx.compile(LoweredProgram(steps=[(2, [[0, 1], [1, 2]])]), 8)
+    assert e.value.code in (3, 9)
+    with pytest.raises(ExecError) as e:
+        ctx.compile(LoweredProgram(steps=[(7, [[0, 1]])]), 8)
+    assert e.value.code == 3
+    # an empty program is a valid no-op (RunLowered returns the initial state)
+    ctx.compile(LoweredProgram(steps=[]), 8)

@@ -1,0 +1,147 @@
+"""Host planner parity: our C++ planner (csrc/planner) against the reference.
+
+* golden program sets / report hashes generated from the UNMODIFIED reference
+  (tests/golden/make_golden.py) — run everywhere;
+* live byte comparison and the reference's own GTest suites compiled against
+  our headers/library — run where /root/reference exists (build container).
+"""
+import hashlib
+import os
+import subprocess
+
+import pytest
+
+from common import GOLDEN, GOLDEN_SETS, ROOT, load_golden
+from paper_2110_10548_b200 import planner
+
+REF_PRESENT = os.path.isdir("/root/reference/proj")
+
+
+def _cfg_path(cfg):
+    return cfg if cfg.startswith("/") else os.path.join(ROOT, cfg)
+
+
+def _available(cfg):
+    return os.path.exists(_cfg_path(cfg))
+
+
+@pytest.mark.parametrize("name", GOLDEN_SETS)
+def test_synthesized_programs_match_reference(name):
+    doc = load_golden(name)
+    c = doc["config"]
+    if not _available(c["system"]):
+        pytest.skip("config file not present on this machine")
+    syn = planner.synthesize(_cfg_path(c["system"]), c["axes"], c["reduce"], payload_bytes=c["payload_bytes"])
+    assert syn.device_count == doc["device_count"]
+    assert len(syn.placements) == len(doc["matrices"])
+    for ours, ref in zip(syn.placements, doc["matrices"]):
+        assert ours.factors == ref["factors"]
+        assert ours.partition == ref["partition"]
+        assert ours.hierarchy == ref["hierarchy"]
+        assert [p.text for p in ours.programs] == [p["text"] for p in ref["programs"]]
+        for p, q in zip(ours.programs, ref["programs"]):
+            assert [(op, [list(g) for g in gs]) for op, gs in p.steps] == \
+                [(s["op"], s["groups"]) for s in q["steps"]]
+            assert p.seconds == q["seconds"]  # bit-identical doubles
+
+
+@pytest.mark.parametrize("name", GOLDEN_SETS)
+def test_report_bytes_match_reference(name):
+    doc = load_golden(name)
+    c = doc["config"]
+    if not _available(c["system"]):
+        pytest.skip("config file not present on this machine")
+    text = planner.report(_cfg_path(c["system"]), c["axes"], c["reduce"], c["payload_bytes"])
+    digest, size = open(os.path.join(GOLDEN, f"report_{name}.sha256")).read().split()
+    assert len(text.encode()) == int(size)
+    assert hashlib.sha256(text.encode()).hexdigest() == digest
+
+
+def test_program_counts_of_baseline_configs():
+    # config 1 = 2 x 4, config 2 = 254 + 500, config 3 = 1,548.
+    counts = {n: sum(len(m["programs"]) for m in load_golden(n)["matrices"]) for n in GOLDEN_SETS}
+    assert counts["cfg1"] == 8
+    assert counts["cfg2_r1"] == 254 and counts["cfg2_r01"] == 500
+    assert sum(counts[f"cfg3_{r}"] for r in ("r0", "r1", "r2", "r01", "r02", "r12")) == 1548
+
+
+def test_baseline_program_present_everywhere():
+    for name in GOLDEN_SETS:
+        for m in load_golden(name)["matrices"]:
+            assert m["programs"][0]["text"] == "Slice(root) InsideGroup AllReduce"
+
+
+def test_refusals_match_reference_runlowered():
+    import json
+    cases = json.load(open(os.path.join(GOLDEN, "refusals.json")))
+    refused = 0
+    for c in cases:
+        prog = planner.LoweredProgram(steps=[(op, gs) for op, gs in c["steps"]])
+        if c["code"] == 0:
+            st = planner.run_lowered(prog, 8)
+            held = [[int(sum(int(b) << col for col, b in enumerate(st[d, r]))) for r in range(8)]
+                    for d in range(8)]
+            assert held == c["held"]
+        else:
+            refused += 1
+            with pytest.raises(planner.RuleViolationError) as e:
+                planner.run_lowered(prog, 8)
+            assert e.value.code == c["code"]
+            assert e.value.step == c["step"] and e.value.violation == c["violation"]
+            assert e.value.message == c["message"]
+    assert refused > 100
+
+
+def test_cli_matches_reference_bytes(tmp_path):
+    exe = os.path.join(ROOT, "paper_2110_10548_b200", "_lib", "synth")
+    out = tmp_path / "r.json"
+    subprocess.check_call([exe, "--system", os.path.join(ROOT, "configs/b200_sock.json"), "--axes", "2,4",
+                           "--reduce", "1", "--bytes", str(256 << 20), "--out", str(out)])
+    digest, size = open(os.path.join(GOLDEN, "report_cfg2_r1.sha256")).read().split()
+    assert hashlib.sha256(out.read_bytes()).hexdigest() == digest
+
+
+def test_cli_error_provenance(tmp_path):
+    exe = os.path.join(ROOT, "paper_2110_10548_b200", "_lib", "synth")
+    r = subprocess.run([exe, "--system", str(tmp_path / "missing.json"), "--axes", "2", "--reduce", "0",
+                        "--bytes", "1"], capture_output=True, text=True)
+    assert r.returncode == 1 and "topology:" in r.stderr
+    r = subprocess.run([exe, "--system", os.path.join(ROOT, "configs/b200_flat2.json"), "--axes", "3",
+                        "--reduce", "0", "--bytes", "1"], capture_output=True, text=True)
+    assert r.returncode == 1 and "placement:" in r.stderr
+
+
+@pytest.mark.skipif(not REF_PRESENT, reason="/root/reference not present (GPU box)")
+@pytest.mark.parametrize("csv", [False, True])
+def test_live_report_identical_to_reference(csv):
+    from oracle import ref
+    if not ref.available():
+        subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "ref"])
+    for cfg, axes, red, payload in [
+        ("configs/b200_sock.json", [2, 4], [0, 1], 1 << 28),
+        ("/root/reference/proj/configs/v100_2node.json", [4, 4], [0], 1 << 32),
+        ("/root/reference/proj/configs/a100_4node.json", [16, 4], [1], 1 << 30),
+    ]:
+        for algo in ("ring", "tree"):
+            ours = planner.report(_cfg_path(cfg), axes, red, payload, algo=algo, fmt="csv" if csv else "json")
+            theirs = ref.report(_cfg_path(cfg), axes, red, payload, algo=1 if algo == "tree" else 0, csv=csv)
+            assert ours == theirs
+
+
+@pytest.mark.skipif(not REF_PRESENT, reason="/root/reference not present (GPU box)")
+def test_reference_gtest_suites_pass_against_our_planner():
+    """The reference's own module suites + acceptance checklist, compiled
+    unmodified against include/redsynth/*.h and libredsynth_planner.a."""
+    subprocess.check_call(["make", "-s", "-C", ROOT, "planner"])
+    subprocess.check_call(["make", "-s", "-j8", "-C", os.path.join(ROOT, "oracle"), "mine-tests"])
+    out_dir = os.path.join(ROOT, "oracle", "_ref")
+    for suite in ["topology", "placement", "semantics", "hierarchy", "dsl", "synthesizer", "simulator",
+                  "report"]:
+        r = subprocess.run([os.path.join(out_dir, f"mine_{suite}_test")], capture_output=True, text=True)
+        assert r.returncode == 0, r.stdout[-3000:]
+    # Acceptance: criterion 5 is red in the reference itself (proj/README.md:118-127).
+    r = subprocess.run([os.path.join(out_dir, "mine_acceptance_test"),
+                        "--gtest_filter=-Checklist.C5_HierarchyExpressiveness"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout[-3000:]
+    for i in (1, 2, 3, 4, 6, 7, 8, 9):
+        assert f"criterion {i} " in r.stdout and "FAIL" not in r.stdout
