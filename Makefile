@@ -26,7 +26,7 @@ EXEC_OBJS    := $(patsubst $(PKG)/csrc/exec/%.cc,$(LIB)/obj/exec_%.o,$(EXEC_CC))
                 $(patsubst $(PKG)/csrc/exec/%.cu,$(LIB)/obj/cu_%.o,$(EXEC_CU))
 
 .PHONY: all planner exec oracle check-ref clean
-all: planner exec
+all: planner exec $(LIB)/execute_example
 
 planner: $(LIB)/libredsynth_planner.a $(LIB)/synth
 
@@ -52,6 +52,9 @@ $(LIB)/obj/cu_%.o: $(PKG)/csrc/exec/%.cu $(EXEC_HDRS)
 
 $(LIB)/libredsynth_b200.so: $(EXEC_OBJS) $(PLANNER_OBJS)
 	$(NVCC) -ccbin /usr/bin/g++ $(ARCH) -shared -o $@ $^ -Xcompiler -pthread -lcuda
+
+$(LIB)/execute_example: examples/execute_program.cc $(LIB)/libredsynth_b200.so
+	$(CXX) $(CXXFLAGS) $(INC) $(CUDA_INC) -o $@ $< -L$(LIB) -lredsynth_b200 -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN' -Wl,-rpath,/usr/local/cuda/lib64
 
 oracle:
 	$(MAKE) -C oracle numeric ref

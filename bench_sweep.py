@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--programs", default="all", help="'all' or 'first:N'")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--graph", action="store_true",
+                    help="time `iters` back-to-back ops captured in one CUDA graph (both arms)")
     args = ap.parse_args()
 
     import torch
@@ -78,6 +80,40 @@ def main():
         t = torch.tensor([us], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
+
+    if args.graph:
+        eager_timed = timed
+
+        def timed(fn):  # noqa: F811 — per-op device time from a graph of `iters` back-to-back ops
+            for _ in range(args.warmup):
+                fn()
+            torch.cuda.synchronize()
+            dist.barrier()
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream(device=dev)
+            s.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    for _ in range(args.iters):
+                        fn()
+            torch.cuda.synchronize()
+            dist.barrier()
+            g.replay()  # warm replay
+            torch.cuda.synchronize()
+            dist.barrier()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            g.replay()
+            b.record(stream)
+            torch.cuda.synchronize()
+            us = a.elapsed_time(b) * 1e3 / args.iters
+            t = torch.tensor([us], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            del g
+            return float(t.item())
+
+        del eager_timed
 
     results = []
     size = args.min

@@ -125,6 +125,9 @@ int rs_plan_step_bytes(rs_plan* plan, int step, double* link_bytes, double* hbm_
 
 /* Tuning knobs (0 = default): CTAs per launch cap and threads per CTA. */
 int rs_plan_set_launch(rs_plan* plan, int max_ctas, int threads);
+/* Named knobs: "unroll" (4|8 vectors in flight per thread per source),
+ * "threads" (per CTA), "max_ctas" (per launch, 0 = resident capacity). */
+int rs_plan_set_option(rs_plan* plan, const char* key, long long value);
 
 /* JSON dump of the compiled plan: per step, per rank, the entry-barrier
  * ranks and tasks {lo, hi (bytes), vec, src slots, dst slots}. */

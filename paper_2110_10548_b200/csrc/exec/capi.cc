@@ -158,10 +158,29 @@ int rs_plan_step_bytes(rs_plan* plan, int step, double* link_bytes, double* hbm_
 
 int rs_plan_set_launch(rs_plan* plan, int max_ctas, int threads) {
   if (!plan) return Bad("null plan");
-  if (threads != 0 && threads != plan->impl->threads) {
-    return Bad("threads is fixed at compile time (512) in this build");
+  if (threads != 0 && (threads < 32 || threads > 512 || threads % 32 != 0)) {
+    return Bad("threads must be a multiple of 32 in [32, 512]");
   }
+  if (threads != 0) plan->impl->threads = threads;
   plan->impl->max_ctas = max_ctas < 0 ? 0 : max_ctas;
+  plan->impl->ctas_per_sm = 0;
+  return RS_OK;
+}
+
+int rs_plan_set_option(rs_plan* plan, const char* key, long long value) {
+  if (!plan || !key) return Bad("null argument");
+  const std::string k(key);
+  if (k == "unroll") {
+    if (value != 4 && value != 8) return Bad("unroll must be 4 or 8");
+    plan->impl->unroll = static_cast<int>(value);
+  } else if (k == "threads") {
+    return rs_plan_set_launch(plan, plan->impl->max_ctas, static_cast<int>(value));
+  } else if (k == "max_ctas") {
+    plan->impl->max_ctas = value < 0 ? 0 : static_cast<int>(value);
+  } else {
+    return Bad("unknown option (unroll | threads | max_ctas)");
+  }
+  plan->impl->ctas_per_sm = 0;
   return RS_OK;
 }
 

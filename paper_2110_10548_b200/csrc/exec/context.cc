@@ -46,6 +46,8 @@ absl::Status AllocateRank(Context* ctx, int r) {
   RS_CUDA(cudaMalloc(&heap, rank.heap_bytes));
   rank.heap = static_cast<char*>(heap);
   RS_CUDA(cudaMemset(rank.heap, 0, kDataOffset));
+  const uint64_t first_epoch = 1;
+  RS_CUDA(cudaMemcpy(rank.heap + kEpochOffset, &first_epoch, sizeof(first_epoch), cudaMemcpyHostToDevice));
   RS_CUDA(cudaStreamCreateWithFlags(&rank.stream, cudaStreamNonBlocking));
   RS_CUDA(cudaDeviceGetAttribute(&rank.sm_count, cudaDevAttrMultiProcessorCount, rank.ordinal));
   rank.driven = true;

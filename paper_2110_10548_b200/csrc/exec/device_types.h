@@ -43,14 +43,21 @@ struct StepArgs {
   uint32_t pad;
   uint8_t wait_ranks[RS_MAX_RANKS];
   uint8_t final_ranks[RS_MAX_RANKS];
-  uint64_t start_value;   // != 0: first step, publish "inputs ready" first
-  uint64_t wait_value;    // wait until inbox[q] >= wait_value for q in wait_ranks
-  uint64_t signal_value;  // published once every CTA finished its pieces
-  uint64_t final_value;   // last step: then wait for final_ranks to reach it
+  // Epochs are relative to a device-resident run base (so a captured CUDA
+  // graph can be replayed): step s waits for base + s, publishes base + s + 1;
+  // step 0 first publishes base ("inputs in place"); the last step waits the
+  // tail barrier for base + num_steps and then advances base by num_steps + 1.
+  uint64_t* epoch_base;
+  uint32_t step;
+  uint32_t num_steps;
   uint64_t timeout_ns;
 };
 
-cudaError_t LaunchStep(const StepArgs& args, int grid, int block, cudaStream_t stream);
+// Vector work is cut into pieces of kPieceBytes; a CTA walks a piece in
+// chunks of threads * unroll * 16 bytes.
+constexpr uint32_t kPieceBytes = 64u << 10;
+
+cudaError_t LaunchStep(const StepArgs& args, int grid, int block, int unroll, cudaStream_t stream);
 
 }  // namespace rs
 

@@ -22,6 +22,7 @@ namespace rs {
 constexpr size_t kInboxOffset = 0;
 constexpr size_t kCounterOffset = 256;
 constexpr size_t kErrorOffset = 512;
+constexpr size_t kEpochOffset = 768;  // uint64 run base epoch (starts at 1)
 constexpr size_t kDataOffset = 4096;
 constexpr size_t kSlotAlign = 1 << 21;  // 2 MiB: keeps every slot buffer 16 B (and page) aligned
 
@@ -32,7 +33,6 @@ struct Rank {
   size_t heap_bytes = 0;
   cudaStream_t stream = nullptr;
   std::vector<char*> view;  // view[q] = rank q's heap as addressed from this rank
-  int max_ctas = 0;         // resident CTA capacity for the step kernel
   int sm_count = 0;
 };
 
@@ -48,7 +48,6 @@ class Context {
   std::vector<int> slot_rank;      // slot -> rank
   std::vector<int> slot_position;  // slot -> index among its rank's slots
   std::vector<Rank> ranks;
-  uint64_t epoch = 1;              // next run's base epoch (identical on all ranks)
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
 
   size_t SlotOffset(int slot) const { return kDataOffset + slot_position[slot] * slot_stride; }
@@ -74,7 +73,9 @@ class Plan {
   size_t elems = 0;
   size_t bytes = 0;  // per slot
   int threads = 512;
-  int max_ctas = 0;  // 0 = resident capacity
+  int unroll = 4;     // 4 or 8 vectors in flight per thread per source
+  int max_ctas = 0;   // 0 = resident capacity
+  int ctas_per_sm = 0;  // resident capacity for (dtype, threads, unroll); 0 = recompute
   std::vector<std::vector<RankStep>> steps;  // [step][rank]
   std::vector<uint8_t> final_wait_bits;      // per rank: bitmask of ranks for the tail wait
   // Device copies (per driven rank): all tasks / pointer tables of all steps.
@@ -102,7 +103,7 @@ absl::Status RunPlan(Plan* plan, void* const* device_bufs, void* const* host_buf
 
 std::string DescribePlan(const Plan& plan);
 
-int MaxResidentCtas(int dtype, int threads);  // per SM, from the occupancy API
+int MaxResidentCtas(int dtype, int threads, int unroll);  // per SM, from the occupancy API
 
 absl::Status CudaStatus(cudaError_t err, const char* what);
 

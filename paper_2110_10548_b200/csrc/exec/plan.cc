@@ -340,7 +340,7 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
   plan->dtype = dtype;
   plan->elems = elems;
   plan->bytes = elems * es;
-  const uint32_t piece_bytes = static_cast<uint32_t>(plan->threads) * 4u * 16u;
+  const uint32_t piece_bytes = kPieceBytes;
 
   // 2./3. Tasks per step.
   Compiler comp(ctx, num_steps, elems, es);
@@ -424,9 +424,6 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
                                  cudaMemcpyHostToDevice), "upload ptrs");
       if (!cs.ok()) return cs;
     }
-    if (ctx->ranks[r].max_ctas == 0) {
-      ctx->ranks[r].max_ctas = MaxResidentCtas(dtype, plan->threads) * ctx->ranks[r].sm_count;
-    }
   }
   *out = plan.release();
   return absl::OkStatus();
@@ -458,9 +455,13 @@ absl::Status RunPlan(Plan* plan, void* const* device_bufs, void* const* host_buf
       }
     }
   }
-  const uint64_t base = ctx->epoch;
   const int S = plan->num_steps;
-  const uint32_t piece_bytes = static_cast<uint32_t>(plan->threads) * 4u * 16u;
+  const uint32_t piece_bytes = kPieceBytes;
+  if (plan->ctas_per_sm == 0 && !driven.empty()) {
+    absl::Status st = CudaStatus(cudaSetDevice(ctx->ranks[driven[0]].ordinal), "cudaSetDevice");
+    if (!st.ok()) return st;
+    plan->ctas_per_sm = MaxResidentCtas(plan->dtype, plan->threads, plan->unroll);
+  }
   for (int s = 0; s < S; ++s) {
     for (size_t i = 0; i < driven.size(); ++i) {
       const int r = driven[i];
@@ -489,20 +490,19 @@ absl::Status RunPlan(Plan* plan, void* const* device_bufs, void* const* host_buf
             if (plan->final_wait_bits[r] & (1u << q)) a.final_ranks[a.nfinal++] = static_cast<uint8_t>(q);
         }
       }
-      a.start_value = s == 0 ? base : 0;
-      a.wait_value = base + static_cast<uint64_t>(s);
-      a.signal_value = base + static_cast<uint64_t>(s) + 1;
-      a.final_value = base + static_cast<uint64_t>(S);
-      int cap = plan->max_ctas > 0 ? std::min(plan->max_ctas, rank.max_ctas) : rank.max_ctas;
+      a.epoch_base = reinterpret_cast<uint64_t*>(rank.heap + kEpochOffset);
+      a.step = static_cast<uint32_t>(s);
+      a.num_steps = static_cast<uint32_t>(S);
+      const int resident = plan->ctas_per_sm * rank.sm_count;
+      int cap = plan->max_ctas > 0 ? std::min(plan->max_ctas, resident) : resident;
       if (cap <= 0) cap = 148;
       const int grid = std::max(1, std::min<int>(cap, static_cast<int>(rsx.npieces)));
       absl::Status st = CudaStatus(cudaSetDevice(rank.ordinal), "cudaSetDevice");
       if (!st.ok()) return st;
-      st = CudaStatus(LaunchStep(a, grid, plan->threads, stream_of(i)), "step kernel launch");
+      st = CudaStatus(LaunchStep(a, grid, plan->threads, plan->unroll, stream_of(i)), "step kernel launch");
       if (!st.ok()) return st;
     }
   }
-  if (S > 0) ctx->epoch = base + static_cast<uint64_t>(S) + 1;
   if (device_bufs || host_bufs) {
     for (size_t i = 0; i < driven.size(); ++i) {
       const int r = driven[i];

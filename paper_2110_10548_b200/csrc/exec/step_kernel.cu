@@ -25,8 +25,6 @@
 namespace rs {
 namespace {
 
-constexpr int kUnroll = 4;
-
 __device__ __forceinline__ uint4 LoadStream(const void* p) {
   uint4 v;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -132,9 +130,10 @@ template <> struct AccOf<RS_F32> { using T = F32Acc; };
 template <> struct AccOf<RS_BF16> { using T = BF16Acc; };
 template <> struct AccOf<RS_I32> { using T = I32Acc; };
 
-// One vector piece: bytes [begin, end) of the task, 16-byte aligned.
-template <int DT>
-__device__ __forceinline__ void VectorPiece(const Task& t, void* const* ptrs, uint64_t begin,
+// One block-wide chunk: bytes [begin, end) of the task, 16-byte aligned;
+// thread t handles vectors begin + (u * blockDim + t) * 16, u < kUnroll.
+template <int DT, int kUnroll>
+__device__ __forceinline__ void VectorChunk(const Task& t, void* const* ptrs, uint64_t begin,
                                             uint64_t end) {
   using Acc = typename AccOf<DT>::T;
   uint64_t off[kUnroll];
@@ -206,17 +205,19 @@ __device__ void ScalarTask(const Task& t, void* const* ptrs) {
   }
 }
 
-template <int DT>
-__global__ void __launch_bounds__(1024) StepKernel(const __grid_constant__ StepArgs a) {
+template <int DT, int kUnroll>
+__global__ void __launch_bounds__(512, kUnroll == 4 ? 2 : 1) StepKernel(const __grid_constant__ StepArgs a) {
+  // Run base epoch (device resident; advanced by the previous run's last step).
+  const uint64_t base = a.nsignal ? *reinterpret_cast<volatile uint64_t*>(a.epoch_base) : 0;
   // 1. First step of a run: publish "my inputs are in place" to every peer.
-  if (a.start_value != 0 && blockIdx.x == 0 && threadIdx.x < a.nsignal) {
+  if (a.step == 0 && blockIdx.x == 0 && threadIdx.x < a.nsignal) {
     FenceSys();
-    StoreReleaseSys(a.signal_ptrs[threadIdx.x], a.start_value);
+    StoreReleaseSys(a.signal_ptrs[threadIdx.x], base);
   }
   // 2. Entry barrier: the ranks whose buffers this step touches (and whose
   //    previous-step writers) have finished the previous step.
   if (threadIdx.x < a.nwait) {
-    WaitAtLeast(a.inbox + a.wait_ranks[threadIdx.x], a.wait_value, a.timeout_ns, a.error_flag);
+    WaitAtLeast(a.inbox + a.wait_ranks[threadIdx.x], base + a.step, a.timeout_ns, a.error_flag);
   }
   __syncthreads();
 
@@ -228,7 +229,8 @@ __global__ void __launch_bounds__(1024) StepKernel(const __grid_constant__ StepA
     if (t.vec) {
       const uint64_t begin = t.lo + static_cast<uint64_t>(p - t.piece_begin) * a.piece_bytes;
       const uint64_t end = min(t.hi, begin + a.piece_bytes);
-      VectorPiece<DT>(t, a.ptrs, begin, end);
+      const uint64_t chunk = static_cast<uint64_t>(blockDim.x) * kUnroll * 16u;
+      for (uint64_t c = begin; c < end; c += chunk) VectorChunk<DT, kUnroll>(t, a.ptrs, c, min(end, c + chunk));
     } else {
       ScalarTask<DT>(t, a.ptrs);
     }
@@ -243,25 +245,27 @@ __global__ void __launch_bounds__(1024) StepKernel(const __grid_constant__ StepA
     if (prev == gridDim.x - 1) {
       atomicExch(a.arrive_counter, 0u);
       FenceSys();
-      for (uint32_t q = 0; q < a.nsignal; ++q) StoreReleaseSys(a.signal_ptrs[q], a.signal_value);
+      for (uint32_t q = 0; q < a.nsignal; ++q) StoreReleaseSys(a.signal_ptrs[q], base + a.step + 1);
       // 5. Last step: the run is complete here only once every rank that
-      //    writes into our slots has finished too.
-      for (uint32_t i = 0; i < a.nfinal; ++i) {
-        WaitAtLeast(a.inbox + a.final_ranks[i], a.final_value, a.timeout_ns, a.error_flag);
+      //    writes into our slots has finished too; then advance the base.
+      if (a.step + 1 == a.num_steps) {
+        for (uint32_t i = 0; i < a.nfinal; ++i) {
+          WaitAtLeast(a.inbox + a.final_ranks[i], base + a.num_steps, a.timeout_ns, a.error_flag);
+        }
+        *reinterpret_cast<volatile uint64_t*>(a.epoch_base) = base + a.num_steps + 1;
       }
     }
   }
 }
 
-}  // namespace
-
-int MaxResidentCtas(int dtype, int threads) {
+template <int U>
+int Occupancy(int dtype, int threads) {
   int blocks = 0;
   cudaError_t e = cudaSuccess;
   switch (dtype) {
-    case RS_F32: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_F32>, threads, 0); break;
-    case RS_BF16: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_BF16>, threads, 0); break;
-    default: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_I32>, threads, 0); break;
+    case RS_F32: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_F32, U>, threads, 0); break;
+    case RS_BF16: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_BF16, U>, threads, 0); break;
+    default: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_I32, U>, threads, 0); break;
   }
   if (e != cudaSuccess || blocks < 1) {
     cudaGetLastError();
@@ -270,14 +274,25 @@ int MaxResidentCtas(int dtype, int threads) {
   return blocks;
 }
 
-cudaError_t LaunchStep(const StepArgs& args, int grid, int block, cudaStream_t stream) {
-  switch (args.dtype) {
-    case RS_F32: StepKernel<RS_F32><<<grid, block, 0, stream>>>(args); break;
-    case RS_BF16: StepKernel<RS_BF16><<<grid, block, 0, stream>>>(args); break;
-    case RS_I32: StepKernel<RS_I32><<<grid, block, 0, stream>>>(args); break;
+template <int U>
+cudaError_t Launch(const StepArgs& a, int grid, int block, cudaStream_t stream) {
+  switch (a.dtype) {
+    case RS_F32: StepKernel<RS_F32, U><<<grid, block, 0, stream>>>(a); break;
+    case RS_BF16: StepKernel<RS_BF16, U><<<grid, block, 0, stream>>>(a); break;
+    case RS_I32: StepKernel<RS_I32, U><<<grid, block, 0, stream>>>(a); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
+}
+
+}  // namespace
+
+int MaxResidentCtas(int dtype, int threads, int unroll) {
+  return unroll == 8 ? Occupancy<8>(dtype, threads) : Occupancy<4>(dtype, threads);
+}
+
+cudaError_t LaunchStep(const StepArgs& args, int grid, int block, int unroll, cudaStream_t stream) {
+  return unroll == 8 ? Launch<8>(args, grid, block, stream) : Launch<4>(args, grid, block, stream);
 }
 
 }  // namespace rs

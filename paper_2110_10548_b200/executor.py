@@ -267,5 +267,9 @@ class Plan:
         nat.check(nat.lib().rs_plan_describe_json(self._h, ctypes.byref(out)))
         return json.loads(nat.take_string(out))
 
-    def set_launch(self, max_ctas: int = 0):
-        nat.check(nat.lib().rs_plan_set_launch(self._h, int(max_ctas), 0))
+    def set_launch(self, max_ctas: int = 0, threads: int = 0):
+        nat.check(nat.lib().rs_plan_set_launch(self._h, int(max_ctas), int(threads)))
+
+    def set_option(self, key: str, value: int):
+        """Named launch knobs: unroll (4|8), threads, max_ctas."""
+        nat.check(nat.lib().rs_plan_set_option(self._h, key.encode(), int(value)))

@@ -54,6 +54,36 @@ def _worker(rank, world, port, result_dir):
                         raise AssertionError(f"rank {rank} slot {d} mismatch: {prog.text}")
                 plan.close()
                 dist.barrier()
+        # CUDA-graph replay across processes (device-resident epochs)
+        _, progs = golden_programs("cfg2_r01")
+        N, dt = 2049, numeric.I32
+        inputs = numeric.synthetic_inputs(K, N, dt)
+        for _, _, prog, _ in progs[::125]:
+            plan = ctx.compile(prog, N, dt)
+            torch.cuda.synchronize()
+            dist.barrier()
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    plan.run()
+            torch.cuda.synchronize()
+            for d in ctx.hosted_slots:
+                ctx.write(d, inputs[d])
+            torch.cuda.synchronize()
+            dist.barrier()
+            for _ in range(4):
+                g.replay()
+            ctx.synchronize()
+            want = [x.copy() for x in inputs]
+            for _ in range(4):
+                numeric.execute(prog, K, want, dt)
+            for d in ctx.hosted_slots:
+                if not np.array_equal(ctx.read(d, N * 4), want[d].view(np.uint8)):
+                    raise AssertionError(f"graph replay mismatch rank {rank} slot {d}: {prog.text}")
+            del g
+            plan.close()
+            dist.barrier()
         dist.barrier()
         ctx.close()
         dist.destroy_process_group()

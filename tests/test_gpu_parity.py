@@ -104,6 +104,38 @@ def test_repeated_runs_chain(local8):
         _run(local8, prog, K, 5000, numeric.I32, runs=3)
 
 
+def test_cuda_graph_replay(local8):
+    """plan.run() captured in a CUDA graph and replayed: epochs are device
+    resident, so replays chain exactly like eager runs."""
+    K, progs = golden_programs("cfg2_r01")
+    N = 3001
+    for _, _, prog, _ in progs[::100]:
+        inputs = numeric.synthetic_inputs(K, N, numeric.I32)
+        for d in range(K):
+            local8.write(d, inputs[d])
+        plan = local8.compile(prog, N, "i32")
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            plan.run()  # warm-up outside capture (state advances: counts as run 1)
+            with torch.cuda.graph(g, stream=s):
+                plan.run()
+        torch.cuda.synchronize()
+        for d in range(K):
+            local8.write(d, inputs[d])
+        for _ in range(3):
+            g.replay()
+        local8.synchronize()
+        want = [x.copy() for x in inputs]
+        for _ in range(3):
+            numeric.execute(prog, K, want, numeric.I32)
+        for d in range(K):
+            assert np.array_equal(local8.read(d, N * 4), want[d].view(np.uint8))
+        del g
+        plan.close()
+
+
 def test_user_and_host_buffer_paths(local8):
     K, progs = golden_programs("cfg2_r01")
     N = 10007
@@ -178,3 +210,16 @@ def test_one_slot_per_gpu_small_k():
             _run(ctx, prog, K, 16 << 20, numeric.BF16, runs=3)
     finally:
         ctx.close()
+
+
+def test_cpp_host_example_end_to_end():
+    """C++ host: reference planner API -> redsynth::GpuExecutor::Execute on
+    every config-2 (reduce {0,1}) program, int32 identity checked in C++."""
+    import subprocess
+    from common import ROOT
+    exe = os.path.join(ROOT, "paper_2110_10548_b200", "_lib", "execute_example")
+    r = subprocess.run([exe, os.path.join(ROOT, "configs", "b200_sock.json"), "2,4", "0,1", "4099"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "programs=500 mismatches=0" in r.stdout
+    assert "step 1: Reduce over devices {0,1}: devices hold different chunk sets" in r.stdout
