@@ -89,6 +89,13 @@ int rs_ctx_destroy(rs_ctx* ctx);
 int rs_ctx_buffer(rs_ctx* ctx, int slot, void** device_ptr);
 /* Number of ranks driven by this process and their CUDA ordinals. */
 int rs_ctx_local_ranks(rs_ctx* ctx, int* count, int* ordinals /* RS_MAX_RANKS */);
+/* Context knobs applied to plans compiled afterwards: "push_min_bytes"
+ * (cross-GPU groups moving at least this many bytes use the two-phase
+ * store-only variant; -1 disables it; default 4 MiB, env RS_PUSH_MIN_BYTES)
+ * and "barrier_timeout_ms" (device-side spin limit, default 20 s). Scratch
+ * for the push variant is reserved at creation: min(K, 8) buffers per slot on
+ * multi-GPU contexts (env RS_SCRATCH_REGIONS). */
+int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value);
 /* Blocks until all work enqueued by this context is done; reports a
  * device-side barrier timeout (INTERNAL) if one happened. */
 int rs_ctx_synchronize(rs_ctx* ctx);

@@ -138,7 +138,7 @@ int rs_plan_run_host(rs_plan* plan, void* const* host_bufs, void* const* streams
 
 int rs_plan_launch_count(rs_plan* plan, int* launches) {
   if (!plan || !launches) return Bad("null argument");
-  *launches = plan->impl->num_steps * static_cast<int>(plan->impl->ctx->DrivenRanks().size());
+  *launches = plan->impl->num_phases() * static_cast<int>(plan->impl->ctx->DrivenRanks().size());
   return RS_OK;
 }
 
@@ -147,12 +147,32 @@ int rs_plan_step_bytes(rs_plan* plan, int step, double* link_bytes, double* hbm_
   const rs::Plan* p = plan->impl;
   if (step < 0 || step >= p->num_steps) return Bad("step out of range");
   double link = 0, hbm = 0;
-  for (const rs::RankStep& r : p->steps[step]) {
-    link = std::max(link, std::max(r.tx_bytes, r.rx_bytes));
-    hbm = std::max(hbm, r.hbm_bytes);
+  for (int ph = 0; ph < p->num_phases(); ++ph) {
+    if (p->phase_step[ph] != step) continue;
+    double l = 0, h = 0;
+    for (const rs::RankStep& r : p->phases[ph]) {
+      l = std::max(l, std::max(r.tx_bytes, r.rx_bytes));
+      h = std::max(h, r.hbm_bytes);
+    }
+    link += l;
+    hbm += h;
   }
   if (link_bytes) *link_bytes = link;
   if (hbm_bytes) *hbm_bytes = hbm;
+  return RS_OK;
+}
+
+int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value) {
+  if (!ctx || !key) return Bad("null argument");
+  const std::string k(key);
+  if (k == "push_min_bytes") {
+    ctx->impl->push_min_bytes = value < 0 ? ~0ull : static_cast<uint64_t>(value);
+  } else if (k == "barrier_timeout_ms") {
+    if (value <= 0) return Bad("barrier_timeout_ms must be positive");
+    ctx->impl->timeout_ns = static_cast<uint64_t>(value) * 1000000ull;
+  } else {
+    return Bad("unknown option (push_min_bytes | barrier_timeout_ms)");
+  }
   return RS_OK;
 }
 

@@ -41,7 +41,8 @@ absl::Status AllocateRank(Context* ctx, int r) {
   RS_CUDA(cudaSetDevice(rank.ordinal));
   int hosted = 0;
   for (int d = 0; d < ctx->K; ++d) hosted += ctx->slot_rank[d] == r;
-  rank.heap_bytes = kDataOffset + static_cast<size_t>(hosted) * ctx->slot_stride;
+  rank.heap_bytes =
+      kDataOffset + static_cast<size_t>(hosted) * (1 + ctx->scratch_regions) * ctx->slot_stride;
   void* heap = nullptr;
   RS_CUDA(cudaMalloc(&heap, rank.heap_bytes));
   rank.heap = static_cast<char*>(heap);
@@ -62,16 +63,28 @@ absl::Status CheckCommon(int K, size_t max_bytes) {
   return absl::OkStatus();
 }
 
+// Slot positions within their rank's heap, and the scratch budget: the push
+// variant lands one copy per group member in the owner's scratch, so
+// cross-GPU contexts reserve min(K, 8) regions per slot (RS_SCRATCH_REGIONS
+// overrides; 0 disables the push variant).
 void AssignPositions(Context* ctx) {
   std::vector<int> next(ctx->world, 0);
   ctx->slot_position.assign(ctx->K, 0);
   for (int d = 0; d < ctx->K; ++d) ctx->slot_position[d] = next[ctx->slot_rank[d]]++;
+  ctx->scratch_regions = ctx->is_virtual ? ctx->K : (ctx->world > 1 ? std::min(ctx->K, 8) : 0);
+  if (const char* env = std::getenv("RS_SCRATCH_REGIONS")) {
+    const int v = std::atoi(env);
+    if (v >= 0) ctx->scratch_regions = v;
+  }
 }
 
 void ReadTimeoutEnv(Context* ctx) {
   if (const char* env = std::getenv("RS_BARRIER_TIMEOUT_S")) {
     const double s = std::atof(env);
     if (s > 0) ctx->timeout_ns = static_cast<uint64_t>(s * 1e9);
+  }
+  if (const char* env = std::getenv("RS_PUSH_MIN_BYTES")) {
+    ctx->push_min_bytes = std::strtoull(env, nullptr, 10);
   }
 }
 
@@ -195,6 +208,7 @@ absl::Status CreateVirtualContext(int K, const int* slot_rank, int world, Contex
     }
   }
   AssignPositions(ctx.get());
+  ReadTimeoutEnv(ctx.get());
   ctx->ranks.resize(world);
   *out = ctx.release();
   return absl::OkStatus();

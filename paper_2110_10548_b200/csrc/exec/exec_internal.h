@@ -18,22 +18,34 @@ namespace rs {
 //   [0, 64)        inbox: uint64 epoch per peer rank (written remotely)
 //   [256, 260)     CTA-arrival counter
 //   [512, 516)     barrier-timeout error flag
-//   [4096, ...)    one buffer per hosted slot, kSlotAlign-aligned stride
+//   [768, 776)     run base epoch (device resident, starts at 1)
+//   [4096, ...)    per hosted slot: its buffer, then `scratch_regions`
+//                  scratch buffers (landing zones of the push variant), each
+//                  slot_stride bytes (max_bytes rounded up to 2 MiB)
 constexpr size_t kInboxOffset = 0;
 constexpr size_t kCounterOffset = 256;
 constexpr size_t kErrorOffset = 512;
-constexpr size_t kEpochOffset = 768;  // uint64 run base epoch (starts at 1)
+constexpr size_t kEpochOffset = 768;
 constexpr size_t kDataOffset = 4096;
-constexpr size_t kSlotAlign = 1 << 21;  // 2 MiB: keeps every slot buffer 16 B (and page) aligned
+constexpr size_t kSlotAlign = 1 << 21;
 
 struct Rank {
-  int ordinal = -1;        // CUDA device (meaningful for ranks driven here)
-  bool driven = false;     // launched by this process
-  char* heap = nullptr;    // local device pointer (driven ranks)
+  int ordinal = -1;         // CUDA device (meaningful for ranks driven here)
+  bool driven = false;      // launched by this process
+  char* heap = nullptr;     // local device pointer (driven ranks)
   size_t heap_bytes = 0;
   cudaStream_t stream = nullptr;
   std::vector<char*> view;  // view[q] = rank q's heap as addressed from this rank
   int sm_count = 0;
+};
+
+// A pointer-table entry: slot `slot`'s buffer (region -1) or its scratch
+// region `region`.
+struct Ref {
+  int slot;
+  int region;
+  friend bool operator==(const Ref&, const Ref&) = default;
+  friend auto operator<=>(const Ref&, const Ref&) = default;
 };
 
 class Context {
@@ -41,6 +53,7 @@ class Context {
   int K = 0;
   size_t max_bytes = 0;
   size_t slot_stride = 0;
+  int scratch_regions = 0;  // per slot; the push variant needs >= group size
   int world = 1;
   int self_rank = -1;  // -1: single process drives every rank
   bool peers_open = false;
@@ -49,40 +62,53 @@ class Context {
   std::vector<int> slot_position;  // slot -> index among its rank's slots
   std::vector<Rank> ranks;
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
+  // Cross-GPU sum/copy groups whose data is at least this many bytes use the
+  // two-phase push variant (stores only over NVLink); smaller ones the
+  // one-pass pull-sum-push variant.
+  uint64_t push_min_bytes = 4ull << 20;
 
-  size_t SlotOffset(int slot) const { return kDataOffset + slot_position[slot] * slot_stride; }
-  char* SlotPtr(int viewer, int slot) const {
-    return ranks[viewer].view[slot_rank[slot]] + SlotOffset(slot);
+  size_t SlotOffset(int slot, int region) const {
+    return kDataOffset +
+           (static_cast<size_t>(slot_position[slot]) * (1 + scratch_regions) + 1 + region) * slot_stride;
   }
+  char* RefPtr(int viewer, const Ref& r) const {
+    return ranks[viewer].view[slot_rank[r.slot]] + SlotOffset(r.slot, r.region);
+  }
+  char* SlotPtr(int viewer, int slot) const { return RefPtr(viewer, Ref{slot, -1}); }
   std::vector<int> DrivenRanks() const;
 };
 
+// One rank's share of one launch phase.
 struct RankStep {
   std::vector<Task> tasks;
-  std::vector<int> ptr_slots;  // slot id per pointer-table entry
+  std::vector<Ref> ptr_refs;  // pointer-table entries
   uint32_t npieces = 0;
-  std::vector<uint8_t> wait;   // ranks to wait for before the step
+  std::vector<uint8_t> wait;  // ranks to wait for before the phase
   double tx_bytes = 0, rx_bytes = 0, hbm_bytes = 0;
 };
 
 class Plan {
  public:
   Context* ctx = nullptr;
-  int num_steps = 0;
+  int num_steps = 0;   // program steps
   int dtype = 0;
   size_t elems = 0;
-  size_t bytes = 0;  // per slot
+  size_t bytes = 0;    // per slot
   int threads = 512;
-  int unroll = 4;     // 4 or 8 vectors in flight per thread per source
-  int max_ctas = 0;   // 0 = resident capacity
+  int unroll = 4;      // 4 or 8 vectors in flight per thread per source
+  int max_ctas = 0;    // 0 = resident capacity
   int ctas_per_sm = 0;  // resident capacity for (dtype, threads, unroll); 0 = recompute
-  std::vector<std::vector<RankStep>> steps;  // [step][rank]
-  std::vector<uint8_t> final_wait_bits;      // per rank: bitmask of ranks for the tail wait
-  // Device copies (per driven rank): all tasks / pointer tables of all steps.
+  // Launch phases: a program step is one phase (pull variant) or two (push
+  // variant: scatter into owners' scratch, then reduce + push results).
+  std::vector<std::vector<RankStep>> phases;  // [phase][rank]
+  std::vector<int> phase_step;                // program step of each phase
+  std::vector<uint8_t> final_wait_bits;       // per rank: ranks for the tail wait
+  // Device copies (per driven rank): all tasks / pointer tables of all phases.
   std::vector<Task*> d_tasks;
   std::vector<void**> d_ptrs;
-  std::vector<std::vector<size_t>> task_offset, ptr_offset;  // [rank][step]
+  std::vector<std::vector<size_t>> task_offset, ptr_offset;  // [rank][phase]
 
+  int num_phases() const { return static_cast<int>(phases.size()); }
   ~Plan();
 };
 

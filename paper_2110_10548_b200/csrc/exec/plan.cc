@@ -1,23 +1,27 @@
-// Plan compiler: LoweredProgram (CSR) -> per-(step, rank) task lists.
+// Plan compiler: LoweredProgram (CSR) -> per-(phase, rank) task lists.
 //
 // 1. Replays the reference semantics step by step (redsynth::
 //    ApplyCollectiveInPlace, semantics.cc:259-310, folded as RunLowered does,
 //    dsl.cc:142-164) to learn which rows every slot holds before each step and
 //    to refuse invalid programs with the reference's step/violation.
-// 2. Turns every group of every step into owner tasks (see step_kernel.cu for
-//    the per-collective data movement) over row ranges; row r of a slot buffer
-//    is elements [floor(rN/K), floor((r+1)N/K)).
+// 2. Turns every group of every step into owner tasks over row ranges; row r
+//    of a slot buffer is elements [floor(rN/K), floor((r+1)N/K)) (SURVEY.md
+//    §8(a) a4). Two variants per group:
+//      pull  one phase: owners load (peer) sources, sum, store (peer) results;
+//      push  two phases, only stores cross NVLink: (A) every source writes the
+//            owner's slice into the owner's scratch (sums) or buffer (copies),
+//            (B) owners sum locally and write results to the destinations.
+//    Cross-GPU groups of >= ctx->push_min_bytes use push (SM stores sustain
+//    ~700 GB/s per direction under bidirectional load, loads ~625).
 // 3. Tracks a content id per (slot, row) so copies whose destination already
 //    holds bit-identical data (same id) are skipped — the result is the same
 //    bits the oracle's unconditional overwrite produces.
-// 4. Computes each rank's entry-barrier set (ranks whose buffers it touches
-//    and their previous-step writers) and the tail barrier of the run.
+// 4. Computes each rank's entry-barrier set per phase (ranks whose memory it
+//    touches and their previous-phase writers) and the run's tail barrier.
 #include <algorithm>
 #include <map>
 #include <memory>
-#include <numeric>
 #include <set>
-#include <tuple>
 
 #include "absl/strings/str_format.h"
 #include "exec_internal.h"
@@ -33,11 +37,13 @@ struct Range {
 };
 
 struct ProtoTask {
-  int owner;
+  int owner;  // slot whose rank executes the task
   Range range;
-  std::vector<int> src;  // slots, summation order
-  std::vector<int> dst;  // slots
+  std::vector<Ref> src;  // summation order
+  std::vector<Ref> dst;
 };
+
+Ref Buf(int slot) { return Ref{slot, -1}; }
 
 class RowGeometry {
  public:
@@ -64,15 +70,19 @@ class RowGeometry {
   size_t es_;
 };
 
+uint64_t TotalBytes(const std::vector<Range>& ranges) {
+  uint64_t t = 0;
+  for (const Range& r : ranges) t += r.hi - r.lo;
+  return t;
+}
+
 // Splits the concatenation of `ranges` into k consecutive parts of nearly
 // equal size whose cut points sit on 16-byte buffer offsets (or on range
 // starts), so owners' vector work stays aligned.
 std::vector<std::vector<Range>> SplitEven(const std::vector<Range>& ranges, int k) {
   std::vector<std::vector<Range>> parts(k);
   if (ranges.empty() || k <= 0) return parts;
-  uint64_t total = 0;
-  for (const Range& r : ranges) total += r.hi - r.lo;
-  // Map concatenated coordinate -> aligned concatenated coordinate.
+  const uint64_t total = TotalBytes(ranges);
   auto align = [&](uint64_t c) {
     uint64_t base = 0;
     for (const Range& r : ranges) {
@@ -110,33 +120,74 @@ std::vector<int> HeldRows(const redsynth::StateContext& st, int d) {
   return st.state(d).NonEmptyRows();
 }
 
+// Task lists of the two phases of one program step.
+struct StepTasks {
+  std::vector<ProtoTask> a;  // push scatter phase (empty when nothing pushes)
+  std::vector<ProtoTask> b;  // pull tasks and push reduce/fan-out tasks
+};
+
 struct Compiler {
   Context* ctx;
   int K;
-  int S;
-  size_t es;
   RowGeometry geo;
   std::vector<uint64_t> vid;  // content id of (slot, row)
   uint64_t next_id;
 
-  Compiler(Context* c, int steps, size_t elems, size_t esize)
-      : ctx(c), K(c->K), S(steps), es(esize), geo(elems, c->K, esize), vid(static_cast<size_t>(c->K) * c->K) {
+  Compiler(Context* c, size_t elems, size_t esize)
+      : ctx(c), K(c->K), geo(elems, c->K, esize), vid(static_cast<size_t>(c->K) * c->K) {
     for (size_t i = 0; i < vid.size(); ++i) vid[i] = i + 1;
     next_id = vid.size() + 1;
   }
   uint64_t& Vid(int d, int r) { return vid[static_cast<size_t>(d) * K + r]; }
 
-  void Emit(std::vector<ProtoTask>& out, const std::vector<Range>& ranges,
-            const std::vector<int>& owners, const std::vector<int>& src, const std::vector<int>& dst) {
-    const std::vector<std::vector<Range>> parts = SplitEven(ranges, static_cast<int>(owners.size()));
-    for (size_t j = 0; j < owners.size(); ++j)
-      for (const Range& r : parts[j]) out.push_back(ProtoTask{owners[j], r, src, dst});
+  bool SpansRanks(const std::vector<int>& g) const {
+    for (int d : g)
+      if (ctx->slot_rank[d] != ctx->slot_rank[g[0]]) return true;
+    return false;
+  }
+  bool PushCopies(const std::vector<int>& g, uint64_t bytes) const {
+    return SpansRanks(g) && bytes >= ctx->push_min_bytes && bytes > 0;
+  }
+  bool PushSums(const std::vector<int>& g, uint64_t bytes) const {
+    return PushCopies(g, bytes) && ctx->scratch_regions >= static_cast<int>(g.size());
   }
 
-  // Copies of rows from their holder to every member whose memory differs.
-  void EmitCopies(std::vector<ProtoTask>& out, const std::vector<int>& g,
-                  const std::vector<std::pair<int, int>>& row_holder) {
-    // Key rows by (holder, receivers) so contiguous rows merge into ranges.
+  static void Add(std::vector<ProtoTask>& out, int owner, const std::vector<Range>& ranges,
+                  const std::vector<Ref>& src, const std::vector<Ref>& dst) {
+    for (const Range& r : ranges) out.push_back(ProtoTask{owner, r, src, dst});
+  }
+
+  // Sum over group g (order = g) of `parts[j]` owned by members owner_idx[j],
+  // results stored to dst_of(j).
+  template <typename DstOf>
+  void Sums(StepTasks& out, const std::vector<int>& g, const std::vector<int>& owner_idx,
+            const std::vector<std::vector<Range>>& parts, bool push, DstOf dst_of) {
+    const int n = static_cast<int>(g.size());
+    for (size_t j = 0; j < owner_idx.size(); ++j) {
+      const int p = owner_idx[j];
+      if (parts[j].empty()) continue;
+      std::vector<Ref> src;
+      if (!push) {
+        for (int m : g) src.push_back(Buf(m));
+        Add(out.b, g[p], parts[j], src, dst_of(j));
+        continue;
+      }
+      // (A) member i lands its copy of the part in owner p's scratch region i.
+      for (int i = 0; i < n; ++i) {
+        if (i == p) continue;
+        Add(out.a, g[i], parts[j], {Buf(g[i])}, {Ref{g[p], i}});
+      }
+      // (B) owner p sums in group order from local memory and stores.
+      for (int i = 0; i < n; ++i) src.push_back(i == p ? Buf(g[p]) : Ref{g[p], i});
+      Add(out.b, g[p], parts[j], src, dst_of(j));
+    }
+  }
+
+  // Copies of rows from their holder to every member whose memory differs
+  // (relay: the receivers own slices; a receiver that pulled — or was pushed —
+  // its slice fans it out to the other receivers).
+  void Copies(StepTasks& out, const std::vector<int>& g,
+              const std::vector<std::pair<int, int>>& row_holder) {
     std::map<std::pair<int, std::vector<int>>, std::vector<int>> by_key;
     for (auto [r, h] : row_holder) {
       std::vector<int> recv;
@@ -145,21 +196,47 @@ struct Compiler {
       if (!recv.empty()) by_key[{h, recv}].push_back(r);
     }
     for (auto& [key, rows] : by_key) {
+      const int h = key.first;
+      const std::vector<int>& recv = key.second;
       std::sort(rows.begin(), rows.end());
-      Emit(out, geo.Ranges(rows), key.second, {key.first}, key.second);
+      const std::vector<Range> ranges = geo.Ranges(rows);
+      std::vector<int> all = recv;
+      all.push_back(h);
+      const bool push = PushCopies(all, TotalBytes(ranges));
+      const std::vector<std::vector<Range>> parts = SplitEven(ranges, static_cast<int>(recv.size()));
+      for (size_t j = 0; j < recv.size(); ++j) {
+        if (parts[j].empty()) continue;
+        std::vector<Ref> others;
+        for (int m : recv)
+          if (m != recv[j]) others.push_back(Buf(m));
+        if (push) {
+          Add(out.a, h, parts[j], {Buf(h)}, {Buf(recv[j])});
+          if (!others.empty()) Add(out.b, recv[j], parts[j], {Buf(recv[j])}, others);
+        } else {
+          std::vector<Ref> dst;
+          for (int m : recv) dst.push_back(Buf(m));
+          Add(out.b, recv[j], parts[j], {Buf(h)}, dst);
+        }
+      }
       for (int r : rows)
-        for (int m : key.second) Vid(m, r) = Vid(key.first, r);
+        for (int m : recv) Vid(m, r) = Vid(h, r);
     }
   }
 
-  void Group(std::vector<ProtoTask>& out, const redsynth::StateContext& pre,
-             const std::vector<int>& g, redsynth::Collective op) {
+  void Group(StepTasks& out, const redsynth::StateContext& pre, const std::vector<int>& g,
+             redsynth::Collective op) {
     using redsynth::Collective;
     const int n = static_cast<int>(g.size());
     switch (op) {
       case Collective::kAllReduce: {
         const std::vector<int> rows = HeldRows(pre, g[0]);
-        Emit(out, geo.Ranges(rows), g, g, g);
+        const std::vector<Range> ranges = geo.Ranges(rows);
+        std::vector<int> owners(n);
+        for (int i = 0; i < n; ++i) owners[i] = i;
+        std::vector<Ref> all;
+        for (int m : g) all.push_back(Buf(m));
+        Sums(out, g, owners, SplitEven(ranges, n), PushSums(g, TotalBytes(ranges)),
+             [&](size_t) { return all; });
         for (int r : rows) {
           const uint64_t id = next_id++;
           for (int m : g) Vid(m, r) = id;
@@ -169,17 +246,26 @@ struct Compiler {
       case Collective::kReduceScatter: {
         const std::vector<int> rows = HeldRows(pre, g[0]);
         const int run = n ? static_cast<int>(rows.size()) / n : 0;
-        for (int m = 0; m < n && run > 0; ++m) {
-          std::vector<int> mine(rows.begin() + m * run, rows.begin() + (m + 1) * run);
-          Emit(out, geo.Ranges(mine), {g[m]}, g, {g[m]});
-          for (int r : mine) Vid(g[m], r) = next_id++;
+        if (run == 0) break;
+        std::vector<int> owners(n);
+        std::vector<std::vector<Range>> parts(n);
+        for (int m = 0; m < n; ++m) {
+          owners[m] = m;
+          parts[m] = geo.Ranges(std::vector<int>(rows.begin() + m * run, rows.begin() + (m + 1) * run));
         }
+        Sums(out, g, owners, parts, PushSums(g, TotalBytes(geo.Ranges(rows))),
+             [&](size_t j) { return std::vector<Ref>{Buf(g[j])}; });
+        for (int m = 0; m < n; ++m)
+          for (int i = m * run; i < (m + 1) * run; ++i) Vid(g[m], rows[i]) = next_id++;
         break;
       }
       case Collective::kReduce: {
         const std::vector<int> rows = HeldRows(pre, g[0]);
-        const std::vector<int> owners(g.begin() + 1, g.end());
-        Emit(out, geo.Ranges(rows), owners, g, {g[0]});
+        const std::vector<Range> ranges = geo.Ranges(rows);
+        std::vector<int> owners;
+        for (int i = 1; i < n; ++i) owners.push_back(i);
+        Sums(out, g, owners, SplitEven(ranges, n - 1), PushSums(g, TotalBytes(ranges)),
+             [&](size_t) { return std::vector<Ref>{Buf(g[0])}; });
         for (int r : rows) Vid(g[0], r) = next_id++;
         break;
       }
@@ -188,13 +274,13 @@ struct Compiler {
         for (int r = 0; r < K; ++r)
           for (int m : g)
             if (!pre.state(m).RowEmpty(r)) row_holder.push_back({r, m});
-        EmitCopies(out, g, row_holder);
+        Copies(out, g, row_holder);
         break;
       }
       case Collective::kBroadcast: {
         std::vector<std::pair<int, int>> row_holder;
         for (int r : HeldRows(pre, g[0])) row_holder.push_back({r, g[0]});
-        EmitCopies(out, g, row_holder);
+        Copies(out, g, row_holder);
         break;
       }
     }
@@ -204,16 +290,16 @@ struct Compiler {
 void AddTraffic(std::vector<RankStep>& per_rank, const Context& ctx, const ProtoTask& t) {
   const double b = static_cast<double>(t.range.hi - t.range.lo);
   const int o = ctx.slot_rank[t.owner];
-  for (int x : t.src) {
-    const int rx = ctx.slot_rank[x];
+  for (const Ref& x : t.src) {
+    const int rx = ctx.slot_rank[x.slot];
     per_rank[rx].hbm_bytes += b;
     if (rx != o) {
       per_rank[o].rx_bytes += b;
       per_rank[rx].tx_bytes += b;
     }
   }
-  for (int y : t.dst) {
-    const int ry = ctx.slot_rank[y];
+  for (const Ref& y : t.dst) {
+    const int ry = ctx.slot_rank[y.slot];
     per_rank[ry].hbm_bytes += b;
     if (ry != o) {
       per_rank[o].tx_bytes += b;
@@ -222,7 +308,7 @@ void AddTraffic(std::vector<RankStep>& per_rank, const Context& ctx, const Proto
   }
 }
 
-// Appends `t` to its owner rank's step: vector body + scalar head/tail.
+// Appends `t` to its owner rank's phase: vector body + scalar head/tail.
 void Lay(RankStep& rs, const ProtoTask& t, uint32_t piece_bytes) {
   auto push = [&](uint64_t lo, uint64_t hi, bool vec) {
     if (hi <= lo) return;
@@ -230,12 +316,12 @@ void Lay(RankStep& rs, const ProtoTask& t, uint32_t piece_bytes) {
     task.lo = lo;
     task.hi = hi;
     task.piece_begin = rs.npieces;
-    task.ptr_begin = static_cast<uint32_t>(rs.ptr_slots.size());
+    task.ptr_begin = static_cast<uint32_t>(rs.ptr_refs.size());
     task.nsrc = static_cast<uint16_t>(t.src.size());
     task.ndst = static_cast<uint16_t>(t.dst.size());
     task.vec = vec ? 1u : 0u;
-    rs.ptr_slots.insert(rs.ptr_slots.end(), t.src.begin(), t.src.end());
-    rs.ptr_slots.insert(rs.ptr_slots.end(), t.dst.begin(), t.dst.end());
+    rs.ptr_refs.insert(rs.ptr_refs.end(), t.src.begin(), t.src.end());
+    rs.ptr_refs.insert(rs.ptr_refs.end(), t.dst.begin(), t.dst.end());
     rs.npieces += vec ? static_cast<uint32_t>((hi - lo + piece_bytes - 1) / piece_bytes) : 1u;
     rs.tasks.push_back(task);
   };
@@ -251,6 +337,12 @@ void Lay(RankStep& rs, const ProtoTask& t, uint32_t piece_bytes) {
   push(t.range.lo, a, false);
   push(a, b, true);
   push(b, t.range.hi, false);
+}
+
+absl::Status Upload(const void* host, size_t bytes, void** dev, const char* what) {
+  absl::Status s = CudaStatus(cudaMalloc(dev, bytes), what);
+  if (!s.ok()) return s;
+  return CudaStatus(cudaMemcpy(*dev, host, bytes, cudaMemcpyHostToDevice), what);
 }
 
 }  // namespace
@@ -340,49 +432,54 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
   plan->dtype = dtype;
   plan->elems = elems;
   plan->bytes = elems * es;
-  const uint32_t piece_bytes = kPieceBytes;
 
-  // 2./3. Tasks per step.
-  Compiler comp(ctx, num_steps, elems, es);
+  // 2./3. Tasks per step, laid out into one or two phases.
+  Compiler comp(ctx, elems, es);
   const int R = ctx->world;
-  plan->steps.assign(num_steps, std::vector<RankStep>(R));
-  // group index of each slot per step (-1 = idle)
-  std::vector<std::vector<int>> gidx(num_steps, std::vector<int>(K, -1));
+  std::vector<std::vector<int>> gidx(num_steps, std::vector<int>(K, -1));  // -1 = idle
   for (int s = 0; s < num_steps; ++s) {
-    std::vector<ProtoTask> tasks;
+    StepTasks tasks;
     const redsynth::CollectiveStep& step = lowered.steps[s];
     for (size_t gi = 0; gi < step.groups.size(); ++gi) {
       for (int d : step.groups[gi]) gidx[s][d] = static_cast<int>(gi);
       comp.Group(tasks, pre[s], step.groups[gi], step.op);
     }
-    for (const ProtoTask& t : tasks) {
-      AddTraffic(plan->steps[s], *ctx, t);
-      Lay(plan->steps[s][ctx->slot_rank[t.owner]], t, piece_bytes);
+    for (const std::vector<ProtoTask>* list : {&tasks.a, &tasks.b}) {
+      if (list == &tasks.a && list->empty()) continue;
+      plan->phases.emplace_back(R);
+      plan->phase_step.push_back(s);
+      for (const ProtoTask& t : *list) {
+        AddTraffic(plan->phases.back(), *ctx, t);
+        Lay(plan->phases.back()[ctx->slot_rank[t.owner]], t, kPieceBytes);
+      }
     }
   }
 
-  // 4. Barrier sets.
-  auto group_of = [&](int s, int d) -> std::vector<int> {
-    if (s < 0 || gidx[s][d] < 0) return {d};
+  // 4. Barrier sets (phases of one step share its groups).
+  const int P = plan->num_phases();
+  auto group_of = [&](int ph, int d) -> std::vector<int> {
+    if (ph < 0) return {d};
+    const int s = plan->phase_step[ph];
+    if (gidx[s][d] < 0) return {d};
     return lowered.steps[s].groups[gidx[s][d]];
   };
   plan->final_wait_bits.assign(R, 0);
-  for (int s = 0; s < num_steps; ++s) {
+  for (int ph = 0; ph < P; ++ph) {
     for (int r = 0; r < R; ++r) {
       std::set<int> wait;
       for (int d = 0; d < K; ++d) {
         if (ctx->slot_rank[d] != r) continue;
-        for (int q : group_of(s, d))
-          for (int p : group_of(s - 1, q)) wait.insert(ctx->slot_rank[p]);
+        for (int q : group_of(ph, d))
+          for (int p : group_of(ph - 1, q)) wait.insert(ctx->slot_rank[p]);
       }
       wait.erase(r);
-      plan->steps[s][r].wait.assign(wait.begin(), wait.end());
+      plan->phases[ph][r].wait.assign(wait.begin(), wait.end());
     }
   }
-  if (num_steps > 0) {
+  if (P > 0) {
     for (int d = 0; d < K; ++d) {
       const int r = ctx->slot_rank[d];
-      for (int p : group_of(num_steps - 1, d)) {
+      for (int p : group_of(P - 1, d)) {
         const int q = ctx->slot_rank[p];
         if (q != r) plan->final_wait_bits[r] |= static_cast<uint8_t>(1u << q);
       }
@@ -392,36 +489,30 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
   // Device copies for every rank this process drives.
   plan->d_tasks.assign(R, nullptr);
   plan->d_ptrs.assign(R, nullptr);
-  plan->task_offset.assign(R, std::vector<size_t>(num_steps, 0));
-  plan->ptr_offset.assign(R, std::vector<size_t>(num_steps, 0));
+  plan->task_offset.assign(R, std::vector<size_t>(P, 0));
+  plan->ptr_offset.assign(R, std::vector<size_t>(P, 0));
   for (int r : ctx->DrivenRanks()) {
     std::vector<Task> all_tasks;
     std::vector<void*> all_ptrs;
-    for (int s = 0; s < num_steps; ++s) {
-      const RankStep& rsx = plan->steps[s][r];
-      plan->task_offset[r][s] = all_tasks.size();
-      plan->ptr_offset[r][s] = all_ptrs.size();
+    for (int ph = 0; ph < P; ++ph) {
+      const RankStep& rsx = plan->phases[ph][r];
+      plan->task_offset[r][ph] = all_tasks.size();
+      plan->ptr_offset[r][ph] = all_ptrs.size();
       all_tasks.insert(all_tasks.end(), rsx.tasks.begin(), rsx.tasks.end());
-      for (int slot : rsx.ptr_slots) all_ptrs.push_back(ctx->SlotPtr(r, slot));
+      for (const Ref& ref : rsx.ptr_refs) all_ptrs.push_back(ctx->RefPtr(r, ref));
     }
     absl::Status cs = CudaStatus(cudaSetDevice(ctx->ranks[r].ordinal), "cudaSetDevice");
     if (!cs.ok()) return cs;
     if (!all_tasks.empty()) {
       void* p = nullptr;
-      cs = CudaStatus(cudaMalloc(&p, all_tasks.size() * sizeof(Task)), "cudaMalloc(tasks)");
-      if (!cs.ok()) return cs;
+      cs = Upload(all_tasks.data(), all_tasks.size() * sizeof(Task), &p, "upload tasks");
       plan->d_tasks[r] = static_cast<Task*>(p);
-      cs = CudaStatus(cudaMemcpy(p, all_tasks.data(), all_tasks.size() * sizeof(Task),
-                                 cudaMemcpyHostToDevice), "upload tasks");
       if (!cs.ok()) return cs;
     }
     if (!all_ptrs.empty()) {
       void* p = nullptr;
-      cs = CudaStatus(cudaMalloc(&p, all_ptrs.size() * sizeof(void*)), "cudaMalloc(ptrs)");
-      if (!cs.ok()) return cs;
+      cs = Upload(all_ptrs.data(), all_ptrs.size() * sizeof(void*), &p, "upload pointers");
       plan->d_ptrs[r] = static_cast<void**>(p);
-      cs = CudaStatus(cudaMemcpy(p, all_ptrs.data(), all_ptrs.size() * sizeof(void*),
-                                 cudaMemcpyHostToDevice), "upload ptrs");
       if (!cs.ok()) return cs;
     }
   }
@@ -437,42 +528,47 @@ absl::Status RunPlan(Plan* plan, void* const* device_bufs, void* const* host_buf
   auto stream_of = [&](size_t i) {
     return streams ? static_cast<cudaStream_t>(streams[i]) : ctx->ranks[driven[i]].stream;
   };
-  // Copy-in (user device buffers or host buffers) of every hosted slot.
-  if (device_bufs || host_bufs) {
+  auto copy_all = [&](bool in) -> absl::Status {
     for (size_t i = 0; i < driven.size(); ++i) {
       const int r = driven[i];
       absl::Status s = CudaStatus(cudaSetDevice(ctx->ranks[r].ordinal), "cudaSetDevice");
       if (!s.ok()) return s;
       for (int d = 0; d < ctx->K; ++d) {
         if (ctx->slot_rank[d] != r) continue;
-        const void* src = device_bufs ? device_bufs[d] : host_bufs[d];
-        if (!src) return absl::InvalidArgumentError(absl::StrFormat("buffer of slot %d is null", d));
-        s = CudaStatus(cudaMemcpyAsync(ctx->SlotPtr(r, d), src, plan->bytes,
-                                       device_bufs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                                       stream_of(i)),
-                       "copy-in");
+        void* user = device_bufs ? device_bufs[d] : host_bufs[d];
+        if (!user) return absl::InvalidArgumentError(absl::StrFormat("buffer of slot %d is null", d));
+        void* slot = ctx->SlotPtr(r, d);
+        const cudaMemcpyKind kind = device_bufs ? cudaMemcpyDeviceToDevice
+                                    : in        ? cudaMemcpyHostToDevice
+                                                : cudaMemcpyDeviceToHost;
+        s = CudaStatus(cudaMemcpyAsync(in ? slot : user, in ? user : slot, plan->bytes, kind, stream_of(i)),
+                       in ? "copy-in" : "copy-out");
         if (!s.ok()) return s;
       }
     }
+    return absl::OkStatus();
+  };
+  if (device_bufs || host_bufs) {
+    absl::Status s = copy_all(true);
+    if (!s.ok()) return s;
   }
-  const int S = plan->num_steps;
-  const uint32_t piece_bytes = kPieceBytes;
+  const int P = plan->num_phases();
   if (plan->ctas_per_sm == 0 && !driven.empty()) {
     absl::Status st = CudaStatus(cudaSetDevice(ctx->ranks[driven[0]].ordinal), "cudaSetDevice");
     if (!st.ok()) return st;
     plan->ctas_per_sm = MaxResidentCtas(plan->dtype, plan->threads, plan->unroll);
   }
-  for (int s = 0; s < S; ++s) {
+  for (int ph = 0; ph < P; ++ph) {
     for (size_t i = 0; i < driven.size(); ++i) {
       const int r = driven[i];
       const Rank& rank = ctx->ranks[r];
-      const RankStep& rsx = plan->steps[s][r];
+      const RankStep& rsx = plan->phases[ph][r];
       StepArgs a{};
-      a.tasks = plan->d_tasks[r] ? plan->d_tasks[r] + plan->task_offset[r][s] : nullptr;
-      a.ptrs = plan->d_ptrs[r] ? plan->d_ptrs[r] + plan->ptr_offset[r][s] : nullptr;
+      a.tasks = plan->d_tasks[r] ? plan->d_tasks[r] + plan->task_offset[r][ph] : nullptr;
+      a.ptrs = plan->d_ptrs[r] ? plan->d_ptrs[r] + plan->ptr_offset[r][ph] : nullptr;
       a.ntasks = static_cast<uint32_t>(rsx.tasks.size());
       a.npieces = rsx.npieces;
-      a.piece_bytes = piece_bytes;
+      a.piece_bytes = kPieceBytes;
       a.dtype = plan->dtype;
       a.arrive_counter = reinterpret_cast<unsigned int*>(rank.heap + kCounterOffset);
       a.error_flag = reinterpret_cast<int*>(rank.heap + kErrorOffset);
@@ -481,18 +577,17 @@ absl::Status RunPlan(Plan* plan, void* const* device_bufs, void* const* host_buf
       if (ctx->world > 1) {
         for (int q = 0; q < ctx->world; ++q) {
           if (q == r) continue;
-          a.signal_ptrs[a.nsignal++] =
-              reinterpret_cast<uint64_t*>(rank.view[q] + kInboxOffset) + r;
+          a.signal_ptrs[a.nsignal++] = reinterpret_cast<uint64_t*>(rank.view[q] + kInboxOffset) + r;
         }
         for (uint8_t q : rsx.wait) a.wait_ranks[a.nwait++] = q;
-        if (s == S - 1) {
+        if (ph == P - 1) {
           for (int q = 0; q < ctx->world; ++q)
             if (plan->final_wait_bits[r] & (1u << q)) a.final_ranks[a.nfinal++] = static_cast<uint8_t>(q);
         }
       }
       a.epoch_base = reinterpret_cast<uint64_t*>(rank.heap + kEpochOffset);
-      a.step = static_cast<uint32_t>(s);
-      a.num_steps = static_cast<uint32_t>(S);
+      a.step = static_cast<uint32_t>(ph);
+      a.num_steps = static_cast<uint32_t>(P);
       const int resident = plan->ctas_per_sm * rank.sm_count;
       int cap = plan->max_ctas > 0 ? std::min(plan->max_ctas, resident) : resident;
       if (cap <= 0) cap = 148;
@@ -503,50 +598,42 @@ absl::Status RunPlan(Plan* plan, void* const* device_bufs, void* const* host_buf
       if (!st.ok()) return st;
     }
   }
-  if (device_bufs || host_bufs) {
-    for (size_t i = 0; i < driven.size(); ++i) {
-      const int r = driven[i];
-      absl::Status s = CudaStatus(cudaSetDevice(ctx->ranks[r].ordinal), "cudaSetDevice");
-      if (!s.ok()) return s;
-      for (int d = 0; d < ctx->K; ++d) {
-        if (ctx->slot_rank[d] != r) continue;
-        void* dst = device_bufs ? device_bufs[d] : host_bufs[d];
-        s = CudaStatus(cudaMemcpyAsync(dst, ctx->SlotPtr(r, d), plan->bytes,
-                                       device_bufs ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                                       stream_of(i)),
-                       "copy-out");
-        if (!s.ok()) return s;
-      }
-    }
-  }
+  if (device_bufs || host_bufs) return copy_all(false);
   return absl::OkStatus();
 }
 
 std::string DescribePlan(const Plan& plan) {
   nlohmann::ordered_json doc;
   doc["num_steps"] = plan.num_steps;
+  doc["num_phases"] = plan.num_phases();
+  doc["phase_step"] = plan.phase_step;
   doc["bytes"] = plan.bytes;
   doc["world"] = plan.ctx->world;
   doc["slot_rank"] = plan.ctx->slot_rank;
-  nlohmann::ordered_json steps = nlohmann::ordered_json::array();
-  for (int s = 0; s < plan.num_steps; ++s) {
+  doc["scratch_regions"] = plan.ctx->scratch_regions;
+  nlohmann::ordered_json phases = nlohmann::ordered_json::array();
+  for (const std::vector<RankStep>& per_rank : plan.phases) {
     nlohmann::ordered_json ranks = nlohmann::ordered_json::array();
-    for (const RankStep& r : plan.steps[s]) {
+    for (const RankStep& r : per_rank) {
       nlohmann::ordered_json tasks = nlohmann::ordered_json::array();
       for (const Task& t : r.tasks) {
-        std::vector<int> src(r.ptr_slots.begin() + t.ptr_begin, r.ptr_slots.begin() + t.ptr_begin + t.nsrc);
-        std::vector<int> dst(r.ptr_slots.begin() + t.ptr_begin + t.nsrc,
-                             r.ptr_slots.begin() + t.ptr_begin + t.nsrc + t.ndst);
+        std::vector<int> src, dst, src_region, dst_region;
+        for (int i = 0; i < t.nsrc + t.ndst; ++i) {
+          const Ref& ref = r.ptr_refs[t.ptr_begin + i];
+          (i < t.nsrc ? src : dst).push_back(ref.slot);
+          (i < t.nsrc ? src_region : dst_region).push_back(ref.region);
+        }
         tasks.push_back({{"lo", t.lo}, {"hi", t.hi}, {"vec", t.vec}, {"piece_begin", t.piece_begin},
-                         {"src", src}, {"dst", dst}});
+                         {"src", src}, {"dst", dst}, {"src_region", src_region},
+                         {"dst_region", dst_region}});
       }
       std::vector<int> wait(r.wait.begin(), r.wait.end());
       ranks.push_back({{"wait", wait}, {"npieces", r.npieces}, {"tx", r.tx_bytes}, {"rx", r.rx_bytes},
                        {"hbm", r.hbm_bytes}, {"tasks", tasks}});
     }
-    steps.push_back({{"ranks", ranks}});
+    phases.push_back({{"ranks", ranks}});
   }
-  doc["steps"] = std::move(steps);
+  doc["steps"] = std::move(phases);  // launch phases (== program steps without push)
   std::vector<std::vector<int>> final_wait;
   for (uint8_t bits : plan.final_wait_bits) {
     std::vector<int> w;

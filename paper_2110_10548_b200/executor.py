@@ -181,6 +181,11 @@ class Context:
     def hosted_slots(self):
         return sorted(self.slot_ordinal)
 
+    def set_option(self, key: str, value: int):
+        """Context knobs for later compiles: push_min_bytes (-1 = never push),
+        barrier_timeout_ms."""
+        nat.check(nat.lib().rs_ctx_set_option(self._h, key.encode(), int(value)))
+
     def synchronize(self):
         import torch
         for o in self.local_ordinals:

@@ -47,15 +47,28 @@ def simulate_plan(desc, bufs, dtype):
     exactly the step kernel's contract. Returns nothing; bufs are updated."""
     es = 2 if dtype == 1 else 4
     view = {0: np.float32, 1: np.uint16, 2: np.int32}[dtype]
+    scratch = {}
+
+    def mem(slot, region):
+        if region < 0:
+            return bufs[slot]
+        key = (slot, region)
+        if key not in scratch:  # fresh scratch holds garbage: poison it
+            scratch[key] = np.full(bufs[slot].nbytes, 0x5A, dtype=np.uint8).view(bufs[slot].dtype)
+        return scratch[key]
+
     for step in desc["steps"]:
         tasks = [t for r in step["ranks"] for t in r["tasks"]]
-        # hazard check: per slot, written intervals vs every other task's accesses
+        for t in tasks:
+            t.setdefault("src_region", [-1] * len(t["src"]))
+            t.setdefault("dst_region", [-1] * len(t["dst"]))
+        # hazard check: per memory object, written intervals vs every other task's accesses
         acc = {}
         for i, t in enumerate(tasks):
-            for s in t["src"]:
-                acc.setdefault(s, []).append((t["lo"], t["hi"], i, "r"))
-            for d in t["dst"]:
-                acc.setdefault(d, []).append((t["lo"], t["hi"], i, "w"))
+            for s, rg in zip(t["src"], t["src_region"]):
+                acc.setdefault((s, rg), []).append((t["lo"], t["hi"], i, "r"))
+            for d, rg in zip(t["dst"], t["dst_region"]):
+                acc.setdefault((d, rg), []).append((t["lo"], t["hi"], i, "w"))
         for slot, ivs in acc.items():
             ivs.sort()
             for a in range(len(ivs)):
@@ -71,7 +84,7 @@ def simulate_plan(desc, bufs, dtype):
             else:
                 assert t["hi"] - t["lo"] < 16
             lo, hi = t["lo"] // es, t["hi"] // es
-            srcs = [bufs[s].view(view)[lo:hi] for s in t["src"]]
+            srcs = [mem(s, rg).view(view)[lo:hi] for s, rg in zip(t["src"], t["src_region"])]
             if len(srcs) == 1:
                 out = srcs[0].copy()
             elif dtype == 0:
@@ -87,5 +100,5 @@ def simulate_plan(desc, bufs, dtype):
                 out = srcs[0].copy()
                 for x in srcs[1:]:
                     out = (out + x).astype(np.int32)
-            for d in t["dst"]:
-                bufs[d].view(view)[lo:hi] = out
+            for d, rg in zip(t["dst"], t["dst_region"]):
+                mem(d, rg).view(view)[lo:hi] = out

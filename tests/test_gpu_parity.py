@@ -179,9 +179,11 @@ def test_oversize_refused(local8):
 @pytest.mark.multigpu
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("mapping", ["block", "interleave"])
-def test_two_gpus_config2(mapping):
+@pytest.mark.parametrize("push", [False, True])
+def test_two_gpus_config2(mapping, push):
     ords = [d * 2 // 8 for d in range(8)] if mapping == "block" else [d % 2 for d in range(8)]
     ctx = executor.Context.local(8, ords, max_bytes=64 << 20)
+    ctx.set_option("push_min_bytes", 0 if push else -1)
     try:
         for name in ("cfg2_r1", "cfg2_r01"):
             K, progs = golden_programs(name)
@@ -196,12 +198,14 @@ def test_two_gpus_config2(mapping):
 
 @pytest.mark.multigpu
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
-def test_one_slot_per_gpu_small_k():
+@pytest.mark.parametrize("push", [False, True])
+def test_one_slot_per_gpu_small_k(push):
     n = min(NGPU, 8)
     name = {2: "k2_flat", 4: "k4_sock", 8: "k8_sock"}.get(n)
     if name is None:
         pytest.skip("GPU count without a golden set")
     ctx = executor.Context.local(n, list(range(n)), max_bytes=64 << 20)
+    ctx.set_option("push_min_bytes", 0 if push else -1)
     try:
         K, progs = golden_programs(name)
         for _, _, prog, _ in progs:

@@ -28,15 +28,16 @@ MAPPINGS = {
 }
 
 
-def _compile(prog, K, mapping, N, dtype):
+def _compile(prog, K, mapping, N, dtype, push=False):
     slot_rank, world = MAPPINGS[mapping](K)
     ctx = executor.Context.virtual(K, slot_rank, world)
+    ctx.set_option("push_min_bytes", 0 if push else -1)
     plan = ctx.compile(prog, N, dtype)
     return ctx, plan, plan.describe()
 
 
-def _check(prog, K, mapping, N, dtype):
-    ctx, plan, desc = _compile(prog, K, mapping, N, dtype)
+def _check(prog, K, mapping, N, dtype, push=False):
+    ctx, plan, desc = _compile(prog, K, mapping, N, dtype, push)
     inputs = numeric.synthetic_inputs(K, N, dtype)
     want = [x.copy() for x in inputs]
     numeric.execute(prog, K, want, dtype, nthreads=1)
@@ -69,6 +70,40 @@ def test_sampled_programs_other_mappings(mapping, dtype):
         K, progs = golden_programs(name)
         for _, _, prog, _ in rng.sample(progs, min(25, len(progs))):
             _check(prog, K, mapping, rng.choice([8, 15, 64, 257, 1000, 4099]), dtype)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2_r1", "cfg2_r01", "k8_sock"])
+def test_push_variant_every_program_bit_exact(name):
+    """Two-phase store-only variant (scatter into owners' scratch, then
+    reduce + push results): same bits as the oracle, hazard-free, and no task
+    ever reads memory of another GPU."""
+    K, progs = golden_programs(name)
+    for _, _, prog, _ in progs:
+        desc = _check(prog, K, "one_per_gpu", 517, numeric.BF16, push=True)
+        for step in desc["steps"]:
+            for r, rk in enumerate(step["ranks"]):
+                for t in rk["tasks"]:
+                    assert all(desc["slot_rank"][s] == r for s in t["src"]), (prog.text, t)
+
+
+@pytest.mark.parametrize("mapping", ["two_gpus", "four_gpus", "interleaved2"])
+@pytest.mark.parametrize("dtype", [numeric.F32, numeric.I32])
+def test_push_variant_other_mappings(mapping, dtype):
+    rng = random.Random(11)
+    for name in ("cfg2_r01", "cfg3_r02", "cfg3_r12"):
+        K, progs = golden_programs(name)
+        for _, _, prog, _ in rng.sample(progs, min(40, len(progs))):
+            _check(prog, K, mapping, rng.choice([9, 64, 1003, 4099]), dtype, push=True)
+
+
+def test_push_allreduce_traffic_is_store_only():
+    K, progs = golden_programs("k8_flat")
+    prog = progs[0][2]
+    _, plan, desc = _compile(prog, K, "one_per_gpu", 1 << 20, numeric.BF16, push=True)
+    assert desc["num_phases"] == 2 and desc["phase_step"] == [0, 0]
+    link, _ = plan.step_bytes(0)
+    D = (1 << 20) * 2
+    assert abs(link - 2 * 7 / 8 * D) <= 256  # same 2(n-1)/n D per direction, all stores
 
 
 @pytest.mark.parametrize("N", [0, 1, 5, 8, 9, 31, 127])

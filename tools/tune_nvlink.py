@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--program", type=int, default=0)
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--dtype", default="bf16")
+    ap.add_argument("--push", type=int, default=-1, help="1 = push variant, 0 = pull, -1 = default threshold")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -32,6 +33,8 @@ def main():
     es = 2 if args.dtype == "bf16" else 4
     nbytes = args.mib << 20
     ctx = executor.Context.from_process_group(world, list(range(world)), nbytes)
+    if args.push >= 0:
+        ctx.set_option("push_min_bytes", 0 if args.push else -1)
     ctx.buffer(rank, nbytes // es, args.dtype).normal_()
     plan = ctx.compile(prog, nbytes // es, args.dtype)
     stream = torch.cuda.current_stream(dev)
