@@ -329,6 +329,11 @@ def main():
         if us < inst["best_us"]:
             inst["best_us"], inst["best"] = round(us, 2), e["prog"].text
     inst_list = list(instances.values())
+    from paper_2110_10548_b200 import rescore
+    resc = rescore.topk([{"instance": (tuple(e["request"]), e["matrix"]), "index": e["index"],
+                          "sim_seconds": e["prog"].seconds, "measured_us": us, "text": e["prog"].text}
+                         for e, us in zip(entries, prog_us)])
+    sim_topk = {"instances": resc["instances"], "top_k": resc["top_k"], "top_k_tie_aware": resc["top_k_tie_aware"]}
 
     # end to end from pinned host memory (fixed sample)
     e2e = None
@@ -387,6 +392,7 @@ def main():
             "program_us": {"mean": round(statistics.mean(prog_us), 2), "min": round(min(prog_us), 2),
                            "max": round(max(prog_us), 2)},
             "instances": inst_list,
+            "simulator_rescoring": sim_topk,
         }
         print(json.dumps(line), flush=True)
     barrier()
@@ -408,18 +414,22 @@ def cpu_baseline(entries):
         return {"value": None, "unavailable": str(exc)}
     threads = numeric.hardware_threads()
     inputs = numeric.synthetic_inputs(K_SLOTS, ELEMS, numeric.BF16)
-    sample = [entries[0], entries[len(entries) // 2]]
+    # Programs spread over the whole set, run until ~10 s of CPU time.
+    order = [entries[(i * 97) % len(entries)] for i in range(len(entries))]
     t = 0.0
     b = 0.0
-    for e in sample:
+    done = 0
+    while t < 10.0 and done < len(order):
+        e = order[done]
         bufs = [x.copy() for x in inputs]
         t0 = time.perf_counter()
         numeric.execute(e["prog"], K_SLOTS, bufs, numeric.BF16, nthreads=threads)
         t += time.perf_counter() - t0
         b += bus_bytes(e)
+        done += 1
     return {"value": round(b / t / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-            "sample": f"{len(sample)} config-2 programs at full size (8 x 256 MiB bf16): "
-                      f"{sample[0]['prog'].text!r}, {sample[1]['prog'].text!r}",
+            "sample": f"{done} config-2 programs (every 97th of the 754, in order) at full size "
+                      f"(8 x 256 MiB bf16), ~10 s of CPU time",
             "seconds": round(t, 2)}
 
 

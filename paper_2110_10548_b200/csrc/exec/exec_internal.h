@@ -64,8 +64,9 @@ class Context {
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
   // Cross-GPU sum/copy groups whose data is at least this many bytes use the
   // two-phase push variant (stores only over NVLink); smaller ones the
-  // one-pass pull-sum-push variant.
-  uint64_t push_min_bytes = 4ull << 20;
+  // one-pass pull-sum-push variant. Off by default: measured +1.5-3% at K=2
+  // for >= 256 MiB but -25% at K=4 (profiles/r01_tune_push*.log).
+  uint64_t push_min_bytes = ~0ull;
 
   size_t SlotOffset(int slot, int region) const {
     return kDataOffset +
