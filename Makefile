@@ -51,7 +51,7 @@ $(LIB)/obj/cu_%.o: $(PKG)/csrc/exec/%.cu $(EXEC_HDRS)
 	$(NVCC) $(NVFLAGS) $(INC) -c $< -o $@ 2> $(LIB)/obj/cu_$*.ptxas.txt || (cat $(LIB)/obj/cu_$*.ptxas.txt; false)
 
 $(LIB)/libredsynth_b200.so: $(EXEC_OBJS) $(PLANNER_OBJS)
-	$(NVCC) -ccbin /usr/bin/g++ $(ARCH) -shared -o $@ $^ -Xcompiler -pthread -lcuda
+	$(NVCC) -ccbin /usr/bin/g++ $(ARCH) -shared -o $@ $^ -Xcompiler -pthread
 
 $(LIB)/execute_example: examples/execute_program.cc $(LIB)/libredsynth_b200.so
 	$(CXX) $(CXXFLAGS) $(INC) $(CUDA_INC) -o $@ $< -L$(LIB) -lredsynth_b200 -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN' -Wl,-rpath,/usr/local/cuda/lib64

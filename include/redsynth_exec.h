@@ -96,6 +96,21 @@ int rs_ctx_local_ranks(rs_ctx* ctx, int* count, int* ordinals /* RS_MAX_RANKS */
  * for the push variant is reserved at creation: min(K, 8) buffers per slot on
  * multi-GPU contexts (env RS_SCRATCH_REGIONS). */
 int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value);
+
+/* NVLS (NVLink SHARP): with RS_NVLS=1 at context creation the heaps are
+ * cuMemCreate'd (shared across processes as POSIX fds via pidfd_getfd) and
+ * AllReduce groups of >= "nvls_min_group" (default 4) slots on distinct GPUs
+ * run as multimem.ld_reduce + multimem.st through the NVSwitch. The switch
+ * sums in its own order, so f32/bf16 results match the ordered oracle within
+ * tolerance instead of bit for bit (i32 never uses NVLS). Options "nvls"
+ * (0/1) and "nvls_min_group" tune later compiles. */
+int rs_ctx_nvls(rs_ctx* ctx, int* enabled);
+/* Host all-gather used to set up multicast objects collectively in the
+ * one-process-per-GPU mode: fn(send, bytes, recv[world * bytes], user) must
+ * gather `bytes` from every rank in rank order and return 0. Plan compiles
+ * are then collective (every rank compiles the same programs in order). */
+typedef int (*rs_exchange_fn)(const void* send, size_t bytes, void* recv, void* user);
+int rs_ctx_set_exchange(rs_ctx* ctx, rs_exchange_fn fn, void* user);
 /* Blocks until all work enqueued by this context is done; reports a
  * device-side barrier timeout (INTERNAL) if one happened. */
 int rs_ctx_synchronize(rs_ctx* ctx);

@@ -170,9 +170,30 @@ int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value) {
   } else if (k == "barrier_timeout_ms") {
     if (value <= 0) return Bad("barrier_timeout_ms must be positive");
     ctx->impl->timeout_ns = static_cast<uint64_t>(value) * 1000000ull;
+  } else if (k == "nvls") {
+    if (value && !ctx->impl->use_vmm && !ctx->impl->is_virtual) {
+      return Bad("NVLS needs a multicast-capable heap: create the context with RS_NVLS=1");
+    }
+    ctx->impl->nvls = value != 0;
+  } else if (k == "nvls_min_group") {
+    if (value < 2) return Bad("nvls_min_group must be >= 2");
+    ctx->impl->nvls_min_group = static_cast<int>(value);
   } else {
-    return Bad("unknown option (push_min_bytes | barrier_timeout_ms)");
+    return Bad("unknown option (push_min_bytes | barrier_timeout_ms | nvls | nvls_min_group)");
   }
+  return RS_OK;
+}
+
+int rs_ctx_set_exchange(rs_ctx* ctx, rs_exchange_fn fn, void* user) {
+  if (!ctx) return Bad("null argument");
+  ctx->impl->exchange = fn;
+  ctx->impl->exchange_user = user;
+  return RS_OK;
+}
+
+int rs_ctx_nvls(rs_ctx* ctx, int* enabled) {
+  if (!ctx || !enabled) return Bad("null argument");
+  *enabled = ctx->impl->nvls ? 1 : 0;
   return RS_OK;
 }
 

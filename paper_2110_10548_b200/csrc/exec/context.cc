@@ -1,10 +1,20 @@
 // Executor contexts: per-rank heaps (slot buffers + barrier flags), peer
 // mappings (CUDA peer access in one process, CUDA IPC across processes) and
 // streams.
+#include <sys/syscall.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+
+#ifndef SYS_pidfd_open
+#define SYS_pidfd_open 434
+#endif
+#ifndef SYS_pidfd_getfd
+#define SYS_pidfd_getfd 438
+#endif
 
 #include "absl/strings/str_format.h"
 #include "exec_internal.h"
@@ -43,9 +53,22 @@ absl::Status AllocateRank(Context* ctx, int r) {
   for (int d = 0; d < ctx->K; ++d) hosted += ctx->slot_rank[d] == r;
   rank.heap_bytes =
       kDataOffset + static_cast<size_t>(hosted) * (1 + ctx->scratch_regions) * ctx->slot_stride;
-  void* heap = nullptr;
-  RS_CUDA(cudaMalloc(&heap, rank.heap_bytes));
-  rank.heap = static_cast<char*>(heap);
+  if (ctx->use_vmm) {
+    // cuMemCreate'd heap: shareable as a POSIX fd and bindable to multicast.
+    std::vector<int> access{rank.ordinal};
+    if (ctx->self_rank < 0) {
+      for (const Rank& other : ctx->ranks)
+        if (other.ordinal != rank.ordinal) access.push_back(other.ordinal);
+    }
+    absl::Status s = VmmAllocate(rank.ordinal, rank.heap_bytes, access, &rank.vmm);
+    if (!s.ok()) return s;
+    rank.heap_bytes = rank.vmm.bytes;
+    rank.heap = reinterpret_cast<char*>(rank.vmm.va);
+  } else {
+    void* heap = nullptr;
+    RS_CUDA(cudaMalloc(&heap, rank.heap_bytes));
+    rank.heap = static_cast<char*>(heap);
+  }
   RS_CUDA(cudaMemset(rank.heap, 0, kDataOffset));
   const uint64_t first_epoch = 1;
   RS_CUDA(cudaMemcpy(rank.heap + kEpochOffset, &first_epoch, sizeof(first_epoch), cudaMemcpyHostToDevice));
@@ -76,6 +99,18 @@ void AssignPositions(Context* ctx) {
     const int v = std::atoi(env);
     if (v >= 0) ctx->scratch_regions = v;
   }
+}
+
+// NVLS needs a VMM heap; opt in with RS_NVLS=1 (multi-GPU contexts whose
+// GPUs support multicast). Every rank of a job must make the same choice.
+void DecideNvls(Context* ctx, const std::vector<int>& ordinals) {
+  const char* env = std::getenv("RS_NVLS");
+  if (!env || std::atoi(env) == 0 || ctx->world < 2) return;
+  for (int o : ordinals)
+    if (!MulticastSupported(o)) return;
+  ctx->use_vmm = true;
+  ctx->nvls = true;
+  if (const char* g = std::getenv("RS_NVLS_MIN_GROUP")) ctx->nvls_min_group = std::max(2, std::atoi(g));
 }
 
 void ReadTimeoutEnv(Context* ctx) {
@@ -123,6 +158,7 @@ absl::Status CreateContext(int K, const int* ordinals, size_t max_bytes, Context
   AssignPositions(ctx.get());
   ctx->ranks.resize(ctx->world);
   for (int r = 0; r < ctx->world; ++r) ctx->ranks[r].ordinal = rank_ordinal[r];
+  DecideNvls(ctx.get(), rank_ordinal);
   for (int r = 0; r < ctx->world; ++r) {
     absl::Status s = AllocateRank(ctx.get(), r);
     if (!s.ok()) {
@@ -180,6 +216,7 @@ absl::Status CreateRankContext(int K, const int* slot_rank, int world, int rank,
   AssignPositions(ctx.get());
   ctx->ranks.resize(world);
   ctx->ranks[rank].ordinal = ordinal;
+  DecideNvls(ctx.get(), {ordinal});
   absl::Status s = AllocateRank(ctx.get(), rank);
   if (!s.ok()) {
     DestroyContext(ctx.release());
@@ -218,6 +255,15 @@ absl::Status IpcHandle(Context* ctx, void* out) {
   if (ctx->self_rank < 0) return absl::InvalidArgumentError("not a per-rank context");
   Rank& me = ctx->ranks[ctx->self_rank];
   RS_CUDA(cudaSetDevice(me.ordinal));
+  std::memset(out, 0, RS_IPC_HANDLE_BYTES);
+  if (ctx->use_vmm) {
+    VmmShare share{};
+    absl::Status s = VmmExport(me.vmm, &share);
+    if (!s.ok()) return s;
+    static_assert(sizeof(share) <= RS_IPC_HANDLE_BYTES, "share size");
+    std::memcpy(out, &share, sizeof(share));
+    return absl::OkStatus();
+  }
   cudaIpcMemHandle_t h;
   RS_CUDA(cudaIpcGetMemHandle(&h, me.heap));
   static_assert(sizeof(h) == RS_IPC_HANDLE_BYTES, "IPC handle size");
@@ -233,8 +279,19 @@ absl::Status OpenPeers(Context* ctx, const void* handles) {
   const char* bytes = static_cast<const char*>(handles);
   for (int q = 0; q < ctx->world; ++q) {
     if (q == ctx->self_rank) continue;
+    const char* blob = bytes + static_cast<size_t>(q) * RS_IPC_HANDLE_BYTES;
+    if (ctx->use_vmm) {
+      VmmShare share;
+      std::memcpy(&share, blob, sizeof(share));
+      VmmBlock block;
+      absl::Status s = VmmImport(share, me.ordinal, &block);
+      if (!s.ok()) return s;
+      me.imported.push_back(block);
+      me.view[q] = reinterpret_cast<char*>(block.va);
+      continue;
+    }
     cudaIpcMemHandle_t h;
-    std::memcpy(&h, bytes + static_cast<size_t>(q) * RS_IPC_HANDLE_BYTES, sizeof(h));
+    std::memcpy(&h, blob, sizeof(h));
     void* p = nullptr;
     RS_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
     me.view[q] = static_cast<char*>(p);
@@ -266,14 +323,220 @@ absl::Status DestroyContext(Context* ctx) {
     if (!rank.driven) continue;
     cudaSetDevice(rank.ordinal);
     if (rank.stream) cudaStreamSynchronize(rank.stream);
-    if (ctx->self_rank >= 0) {
+    if (ctx->self_rank >= 0 && !ctx->use_vmm) {
       for (int q = 0; q < ctx->world; ++q)
         if (q != r && rank.view.size() > static_cast<size_t>(q) && rank.view[q]) cudaIpcCloseMemHandle(rank.view[q]);
     }
     if (rank.stream) cudaStreamDestroy(rank.stream);
-    if (rank.heap) cudaFree(rank.heap);
+  }
+  // Multicast objects first (they hold bindings to the heaps).
+  for (auto& [slots, mc] : ctx->mc_groups) {
+    for (int r = 0; r < ctx->world; ++r) {
+      if (!ctx->ranks[r].driven || !mc->va[r]) continue;
+      cudaSetDevice(ctx->ranks[r].ordinal);
+      cudaDeviceSynchronize();
+      drv::cuMemUnmap(mc->va[r], mc->bytes);
+      drv::cuMemAddressFree(mc->va[r], mc->bytes);
+      if (ctx->self_rank < 0) break;  // one mapping shared by every device
+    }
+    for (int d : slots) {
+      const int r = ctx->slot_rank[d];
+      if (!ctx->ranks[r].driven) continue;
+      CUdevice dev;
+      if (drv::cuDeviceGet(&dev, ctx->ranks[r].ordinal) == CUDA_SUCCESS) {
+        drv::cuMulticastUnbind(mc->handle, dev, 0, mc->bytes);
+      }
+    }
+    if (mc->handle) drv::cuMemRelease(mc->handle);
+  }
+  for (int r = 0; r < ctx->world; ++r) {
+    Rank& rank = ctx->ranks[r];
+    if (!rank.driven) continue;
+    cudaSetDevice(rank.ordinal);
+    for (VmmBlock& b : rank.imported) VmmRelease(&b);
+    if (ctx->use_vmm) {
+      VmmRelease(&rank.vmm);
+    } else if (rank.heap) {
+      cudaFree(rank.heap);
+    }
   }
   delete ctx;
+  return absl::OkStatus();
+}
+
+namespace {
+
+// Collective host exchange (all ranks, same order): send `bytes` bytes,
+// receive world * bytes. Required for multi-process multicast setup.
+absl::Status Exchange(Context* ctx, const void* send, size_t bytes, std::vector<char>* recv) {
+  recv->assign(bytes * ctx->world, 0);
+  if (ctx->exchange == nullptr) {
+    return absl::FailedPreconditionError(
+        "multi-process NVLS setup needs the host exchange callback (rs_ctx_set_exchange)");
+  }
+  if (ctx->exchange(send, bytes, recv->data(), ctx->exchange_user) != 0) {
+    return absl::InternalError("host exchange callback failed");
+  }
+  return absl::OkStatus();
+}
+
+struct McShare {
+  int32_t pid;
+  int32_t fd;
+  int32_t ok;
+  int32_t pad;
+};
+
+}  // namespace
+
+absl::Status EnsureMulticast(Context* ctx, const std::vector<int>& slots, int* index) {
+  auto found = ctx->mc_groups.find(slots);
+  if (found != ctx->mc_groups.end()) {
+    for (size_t i = 0; i < ctx->mc_index.size(); ++i)
+      if (ctx->mc_index[i] == found->second.get()) *index = static_cast<int>(i);
+    return absl::OkStatus();
+  }
+  auto mc = std::make_unique<McGroup>();
+  mc->slots = slots;
+  mc->va.assign(ctx->world, 0);
+  if (ctx->is_virtual) {  // planning only: record the group, no CUDA objects
+    *index = static_cast<int>(ctx->mc_index.size());
+    ctx->mc_index.push_back(mc.get());
+    ctx->mc_groups[slots] = std::move(mc);
+    return absl::OkStatus();
+  }
+  const int n = static_cast<int>(slots.size());
+  const size_t gran = MulticastGranularity(n, ctx->max_bytes);
+  mc->bytes = (ctx->max_bytes + gran - 1) / gran * gran;
+  if (mc->bytes > ctx->slot_stride) return absl::InternalError("multicast size exceeds slot stride");
+  CUmulticastObjectProp prop = {};
+  prop.numDevices = static_cast<unsigned>(n);
+  prop.size = mc->bytes;
+  prop.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  auto device_of = [&](int r) {
+    CUdevice dev = 0;
+    drv::cuDeviceGet(&dev, ctx->ranks[r].ordinal);
+    return dev;
+  };
+  auto bind_and_map = [&](int r, int slot, const std::vector<int>& access) -> absl::Status {
+    RS_CUDA(cudaSetDevice(ctx->ranks[r].ordinal));
+    absl::Status s = CuStatus(
+        drv::cuMulticastBindMem(mc->handle, 0, ctx->ranks[r].vmm.handle, ctx->SlotOffset(slot, -1), mc->bytes, 0),
+        "cuMulticastBindMem");
+    return s;
+  };
+  auto map_va = [&](const std::vector<int>& access, CUdeviceptr* va) -> absl::Status {
+    absl::Status s = CuStatus(drv::cuMemAddressReserve(va, mc->bytes, gran, 0, 0), "reserve multicast VA");
+    if (!s.ok()) return s;
+    s = CuStatus(drv::cuMemMap(*va, mc->bytes, 0, mc->handle, 0), "map multicast VA");
+    if (!s.ok()) return s;
+    std::vector<CUmemAccessDesc> desc(access.size());
+    for (size_t i = 0; i < access.size(); ++i) {
+      desc[i].location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+      desc[i].location.id = access[i];
+      desc[i].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    }
+    return CuStatus(drv::cuMemSetAccess(*va, mc->bytes, desc.data(), desc.size()), "multicast access");
+  };
+
+  if (ctx->self_rank < 0) {
+    // One process: create, add every member GPU, bind each member's slot
+    // buffer, map one VA usable by all members.
+    absl::Status s = CuStatus(drv::cuMulticastCreate(&mc->handle, &prop), "cuMulticastCreate");
+    if (!s.ok()) return s;
+    std::vector<int> access;
+    for (int d : slots) {
+      const int r = ctx->slot_rank[d];
+      s = CuStatus(drv::cuMulticastAddDevice(mc->handle, device_of(r)), "cuMulticastAddDevice");
+      if (!s.ok()) return s;
+      access.push_back(ctx->ranks[r].ordinal);
+    }
+    for (int d : slots) {
+      s = bind_and_map(ctx->slot_rank[d], d, access);
+      if (!s.ok()) return s;
+    }
+    CUdeviceptr va = 0;
+    s = map_va(access, &va);
+    if (!s.ok()) return s;
+    for (int d : slots) mc->va[ctx->slot_rank[d]] = va;
+  } else {
+    // One process per GPU: the first member's rank creates and shares the
+    // object (fd via pidfd_getfd); every member adds its GPU, then binds its
+    // slot and maps its own VA. All ranks take part in the exchanges.
+    const int me = ctx->self_rank;
+    const int creator = ctx->slot_rank[slots[0]];
+    bool member = false;
+    int my_slot = -1;
+    for (int d : slots) {
+      if (ctx->slot_rank[d] == me) {
+        member = true;
+        my_slot = d;
+      }
+    }
+    McShare mine{};
+    absl::Status s;
+    if (me == creator) {
+      s = CuStatus(drv::cuMulticastCreate(&mc->handle, &prop), "cuMulticastCreate");
+      if (s.ok()) {
+        int fd = -1;
+        s = CuStatus(drv::cuMemExportToShareableHandle(&fd, mc->handle, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0),
+                     "export multicast");
+        mine = McShare{static_cast<int32_t>(getpid()), fd, s.ok() ? 1 : 0, 0};
+      }
+    }
+    std::vector<char> all;
+    absl::Status xs = Exchange(ctx, &mine, sizeof(mine), &all);
+    if (!xs.ok()) return xs;
+    if (!s.ok()) return s;
+    McShare theirs;
+    std::memcpy(&theirs, all.data() + static_cast<size_t>(creator) * sizeof(McShare), sizeof(theirs));
+    if (!theirs.ok) return absl::InternalError("multicast creation failed on the creator rank");
+    int32_t added = 1;
+    if (member && me != creator) {
+      VmmShare vs{kVmmMagic, theirs.pid, theirs.fd, 0, mc->bytes};
+      // Reuse the fd import path (pidfd_getfd) without mapping.
+      const int pidfd = static_cast<int>(syscall(SYS_pidfd_open, vs.pid, 0));
+      const int fd = pidfd < 0 ? -1 : static_cast<int>(syscall(SYS_pidfd_getfd, pidfd, vs.fd, 0));
+      if (pidfd >= 0) close(pidfd);
+      if (fd < 0) {
+        added = 0;
+        s = absl::UnavailableError("pidfd_getfd failed for the multicast handle");
+      } else {
+        s = CuStatus(drv::cuMemImportFromShareableHandle(&mc->handle, reinterpret_cast<void*>(static_cast<intptr_t>(fd)),
+                                                    CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR),
+                     "import multicast");
+        close(fd);
+      }
+    }
+    if (member && s.ok()) {
+      s = CuStatus(drv::cuMulticastAddDevice(mc->handle, device_of(me)), "cuMulticastAddDevice");
+      added = s.ok() ? 1 : 0;
+    }
+    xs = Exchange(ctx, &added, sizeof(added), &all);
+    if (!xs.ok()) return xs;
+    for (int r = 0; r < ctx->world; ++r) {
+      int32_t v;
+      std::memcpy(&v, all.data() + r * sizeof(int32_t), sizeof(v));
+      if (!v) return s.ok() ? absl::InternalError(absl::StrFormat("rank %d failed to join multicast", r)) : s;
+    }
+    int32_t bound = 1;
+    if (member) {
+      s = bind_and_map(me, my_slot, {ctx->ranks[me].ordinal});
+      if (s.ok()) s = map_va({ctx->ranks[me].ordinal}, &mc->va[me]);
+      bound = s.ok() ? 1 : 0;
+    }
+    xs = Exchange(ctx, &bound, sizeof(bound), &all);
+    if (!xs.ok()) return xs;
+    for (int r = 0; r < ctx->world; ++r) {
+      int32_t v;
+      std::memcpy(&v, all.data() + r * sizeof(int32_t), sizeof(v));
+      if (!v) return s.ok() ? absl::InternalError(absl::StrFormat("rank %d failed to bind multicast", r)) : s;
+    }
+    if (me == creator && mine.fd >= 0) close(mine.fd);
+  }
+  *index = static_cast<int>(ctx->mc_index.size());
+  ctx->mc_index.push_back(mc.get());
+  ctx->mc_groups[slots] = std::move(mc);
   return absl::OkStatus();
 }
 

@@ -22,8 +22,13 @@ struct Task {
   uint32_t ptr_begin;    // srcs = ptrs[ptr_begin, +nsrc), dsts follow
   uint16_t nsrc;
   uint16_t ndst;
-  uint32_t vec;
+  uint16_t vec;
+  uint16_t mode;  // kModeSum, or kModeNvlsAllReduce: ptrs[ptr_begin] is a multicast
+                  // base; dst = multimem.ld_reduce(src) written back with multimem.st
 };
+
+constexpr uint16_t kModeSum = 0;
+constexpr uint16_t kModeNvlsAllReduce = 1;
 
 // Everything one rank's kernel for one step needs (passed by value).
 struct StepArgs {
@@ -40,7 +45,7 @@ struct StepArgs {
   uint32_t nsignal;
   uint32_t nwait;
   uint32_t nfinal;
-  uint32_t pad;
+  uint32_t has_nvls;  // any multimem task: order unicast/multicast aliases (fence.proxy.alias)
   uint8_t wait_ranks[RS_MAX_RANKS];
   uint8_t final_ranks[RS_MAX_RANKS];
   // Epochs are relative to a device-resident run base (so a captured CUDA

@@ -3,6 +3,8 @@
 #define REDSYNTH_B200_EXEC_INTERNAL_H_
 
 #include <cstdint>
+#include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -10,6 +12,7 @@
 
 #include "absl/status/status.h"
 #include "device_types.h"
+#include "vmm.h"
 #include "redsynth_exec.h"
 
 namespace rs {
@@ -19,14 +22,14 @@ namespace rs {
 //   [256, 260)     CTA-arrival counter
 //   [512, 516)     barrier-timeout error flag
 //   [768, 776)     run base epoch (device resident, starts at 1)
-//   [4096, ...)    per hosted slot: its buffer, then `scratch_regions`
+//   [2 MiB, ...)   per hosted slot: its buffer, then `scratch_regions`
 //                  scratch buffers (landing zones of the push variant), each
 //                  slot_stride bytes (max_bytes rounded up to 2 MiB)
 constexpr size_t kInboxOffset = 0;
 constexpr size_t kCounterOffset = 256;
 constexpr size_t kErrorOffset = 512;
 constexpr size_t kEpochOffset = 768;
-constexpr size_t kDataOffset = 4096;
+constexpr size_t kDataOffset = 2u << 20;  // multicast-bind granularity
 constexpr size_t kSlotAlign = 1 << 21;
 
 struct Rank {
@@ -37,13 +40,28 @@ struct Rank {
   cudaStream_t stream = nullptr;
   std::vector<char*> view;  // view[q] = rank q's heap as addressed from this rank
   int sm_count = 0;
+  VmmBlock vmm;                   // heap allocation when ctx->use_vmm
+  std::vector<VmmBlock> imported;  // peers' heaps mapped here (multi-process VMM)
 };
+
+// An NVLink multicast object over the slot buffers of one group (one slot per
+// GPU), addressed by multimem.ld_reduce / multimem.st.
+struct McGroup {
+  std::vector<int> slots;
+  CUmemGenericAllocationHandle handle = 0;
+  size_t bytes = 0;
+  std::vector<CUdeviceptr> va;  // per rank: the multicast VA mapped for it (0 = none)
+};
+
+typedef int (*ExchangeFn)(const void* send, size_t bytes, void* recv, void* user);
 
 // A pointer-table entry: slot `slot`'s buffer (region -1) or its scratch
 // region `region`.
+constexpr int kMcRegion = -2;  // Ref{mc group index, kMcRegion}: a multicast base
+
 struct Ref {
-  int slot;
-  int region;
+  int slot;    // slot id, or mc group index for kMcRegion
+  int region;  // -1 buffer, >= 0 scratch region, kMcRegion multicast
   friend bool operator==(const Ref&, const Ref&) = default;
   friend auto operator<=>(const Ref&, const Ref&) = default;
 };
@@ -67,12 +85,24 @@ class Context {
   // one-pass pull-sum-push variant. Off by default: measured +1.5-3% at K=2
   // for >= 256 MiB but -25% at K=4 (profiles/r01_tune_push*.log).
   uint64_t push_min_bytes = ~0ull;
+  // NVLS: AllReduce groups of >= nvls_min_group slots on distinct GPUs use
+  // multimem.ld_reduce + multimem.st through the NVSwitch (needs a VMM heap,
+  // RS_NVLS=1 at creation; sums then follow the switch's order: f32/bf16
+  // results are within tolerance of the ordered oracle, i32 never uses it).
+  bool use_vmm = false;
+  bool nvls = false;
+  int nvls_min_group = 4;
+  ExchangeFn exchange = nullptr;  // host all-gather (multi-process NVLS setup)
+  void* exchange_user = nullptr;
+  std::map<std::vector<int>, std::unique_ptr<McGroup>> mc_groups;
 
   size_t SlotOffset(int slot, int region) const {
     return kDataOffset +
            (static_cast<size_t>(slot_position[slot]) * (1 + scratch_regions) + 1 + region) * slot_stride;
   }
+  std::vector<McGroup*> mc_index;  // Ref{i, kMcRegion} -> group
   char* RefPtr(int viewer, const Ref& r) const {
+    if (r.region == kMcRegion) return reinterpret_cast<char*>(mc_index[r.slot]->va[viewer]);
     return ranks[viewer].view[slot_rank[r.slot]] + SlotOffset(r.slot, r.region);
   }
   char* SlotPtr(int viewer, int slot) const { return RefPtr(viewer, Ref{slot, -1}); }
@@ -121,6 +151,9 @@ absl::Status IpcHandle(Context* ctx, void* out);
 absl::Status OpenPeers(Context* ctx, const void* handles);
 absl::Status DestroyContext(Context* ctx);
 absl::Status Synchronize(Context* ctx);
+// Creates (collectively, in multi-process mode) or finds the multicast object
+// over `slots`; returns its index for Ref{index, kMcRegion}.
+absl::Status EnsureMulticast(Context* ctx, const std::vector<int>& slots, int* index);
 
 absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
                          const int32_t* step_group_ptr, const int32_t* group_member_ptr,

@@ -41,6 +41,7 @@ struct ProtoTask {
   Range range;
   std::vector<Ref> src;  // summation order
   std::vector<Ref> dst;
+  int mc = -1;  // >= 0: NVLS AllReduce through multicast group mc (vector body)
 };
 
 Ref Buf(int slot) { return Ref{slot, -1}; }
@@ -129,12 +130,13 @@ struct StepTasks {
 struct Compiler {
   Context* ctx;
   int K;
+  int dtype;
   RowGeometry geo;
   std::vector<uint64_t> vid;  // content id of (slot, row)
   uint64_t next_id;
 
-  Compiler(Context* c, size_t elems, size_t esize)
-      : ctx(c), K(c->K), geo(elems, c->K, esize), vid(static_cast<size_t>(c->K) * c->K) {
+  Compiler(Context* c, size_t elems, size_t esize, int dt)
+      : ctx(c), K(c->K), dtype(dt), geo(elems, c->K, esize), vid(static_cast<size_t>(c->K) * c->K) {
     for (size_t i = 0; i < vid.size(); ++i) vid[i] = i + 1;
     next_id = vid.size() + 1;
   }
@@ -223,8 +225,19 @@ struct Compiler {
     }
   }
 
-  void Group(StepTasks& out, const redsynth::StateContext& pre, const std::vector<int>& g,
-             redsynth::Collective op) {
+  // NVLS applies to AllReduce groups of >= nvls_min_group slots, one per GPU,
+  // for floating-point data.
+  bool NvlsEligible(const std::vector<int>& g, uint64_t bytes) const {
+    if (!ctx->nvls || dtype == RS_I32 || bytes == 0) return false;
+    if (static_cast<int>(g.size()) < ctx->nvls_min_group) return false;
+    std::vector<int> ranks;
+    for (int d : g) ranks.push_back(ctx->slot_rank[d]);
+    std::sort(ranks.begin(), ranks.end());
+    return std::adjacent_find(ranks.begin(), ranks.end()) == ranks.end();
+  }
+
+  absl::Status Group(StepTasks& out, const redsynth::StateContext& pre, const std::vector<int>& g,
+                     redsynth::Collective op) {
     using redsynth::Collective;
     const int n = static_cast<int>(g.size());
     switch (op) {
@@ -235,8 +248,17 @@ struct Compiler {
         for (int i = 0; i < n; ++i) owners[i] = i;
         std::vector<Ref> all;
         for (int m : g) all.push_back(Buf(m));
-        Sums(out, g, owners, SplitEven(ranges, n), PushSums(g, TotalBytes(ranges)),
-             [&](size_t) { return all; });
+        if (NvlsEligible(g, TotalBytes(ranges))) {
+          int mc = -1;
+          absl::Status s = EnsureMulticast(ctx, g, &mc);
+          if (!s.ok()) return s;
+          const std::vector<std::vector<Range>> parts = SplitEven(ranges, n);
+          for (int p = 0; p < n; ++p)
+            for (const Range& r : parts[p]) out.b.push_back(ProtoTask{g[p], r, all, all, mc});
+        } else {
+          Sums(out, g, owners, SplitEven(ranges, n), PushSums(g, TotalBytes(ranges)),
+               [&](size_t) { return all; });
+        }
         for (int r : rows) {
           const uint64_t id = next_id++;
           for (int m : g) Vid(m, r) = id;
@@ -284,12 +306,27 @@ struct Compiler {
         break;
       }
     }
+    return absl::OkStatus();
   }
 };
 
 void AddTraffic(std::vector<RankStep>& per_rank, const Context& ctx, const ProtoTask& t) {
   const double b = static_cast<double>(t.range.hi - t.range.lo);
   const int o = ctx.slot_rank[t.owner];
+  if (t.mc >= 0) {
+    // Switch reads every member's copy (tx b each), returns the sum to the
+    // owner (rx b); the multicast store leaves the owner (tx b) and lands in
+    // every member (rx b).
+    for (const Ref& x : t.src) {
+      RankStep& m = per_rank[ctx.slot_rank[x.slot]];
+      m.tx_bytes += b;
+      m.rx_bytes += b;
+      m.hbm_bytes += 2 * b;
+    }
+    per_rank[o].rx_bytes += b;
+    per_rank[o].tx_bytes += b;
+    return;
+  }
   for (const Ref& x : t.src) {
     const int rx = ctx.slot_rank[x.slot];
     per_rank[rx].hbm_bytes += b;
@@ -317,9 +354,19 @@ void Lay(RankStep& rs, const ProtoTask& t, uint32_t piece_bytes) {
     task.hi = hi;
     task.piece_begin = rs.npieces;
     task.ptr_begin = static_cast<uint32_t>(rs.ptr_refs.size());
+    task.vec = vec ? 1u : 0u;
+    if (vec && t.mc >= 0) {
+      // NVLS body: one multicast base pointer (unaligned edges stay ordered P2P sums).
+      task.mode = kModeNvlsAllReduce;
+      task.nsrc = 1;
+      task.ndst = 0;
+      rs.ptr_refs.push_back(Ref{t.mc, kMcRegion});
+      rs.npieces += static_cast<uint32_t>((hi - lo + piece_bytes - 1) / piece_bytes);
+      rs.tasks.push_back(task);
+      return;
+    }
     task.nsrc = static_cast<uint16_t>(t.src.size());
     task.ndst = static_cast<uint16_t>(t.dst.size());
-    task.vec = vec ? 1u : 0u;
     rs.ptr_refs.insert(rs.ptr_refs.end(), t.src.begin(), t.src.end());
     rs.ptr_refs.insert(rs.ptr_refs.end(), t.dst.begin(), t.dst.end());
     rs.npieces += vec ? static_cast<uint32_t>((hi - lo + piece_bytes - 1) / piece_bytes) : 1u;
@@ -434,7 +481,7 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
   plan->bytes = elems * es;
 
   // 2./3. Tasks per step, laid out into one or two phases.
-  Compiler comp(ctx, elems, es);
+  Compiler comp(ctx, elems, es, dtype);
   const int R = ctx->world;
   std::vector<std::vector<int>> gidx(num_steps, std::vector<int>(K, -1));  // -1 = idle
   for (int s = 0; s < num_steps; ++s) {
@@ -442,7 +489,8 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
     const redsynth::CollectiveStep& step = lowered.steps[s];
     for (size_t gi = 0; gi < step.groups.size(); ++gi) {
       for (int d : step.groups[gi]) gidx[s][d] = static_cast<int>(gi);
-      comp.Group(tasks, pre[s], step.groups[gi], step.op);
+      absl::Status gs = comp.Group(tasks, pre[s], step.groups[gi], step.op);
+      if (!gs.ok()) return gs;
     }
     for (const std::vector<ProtoTask>* list : {&tasks.a, &tasks.b}) {
       if (list == &tasks.a && list->empty()) continue;
@@ -588,6 +636,7 @@ absl::Status RunPlan(Plan* plan, void* const* device_bufs, void* const* host_buf
       a.epoch_base = reinterpret_cast<uint64_t*>(rank.heap + kEpochOffset);
       a.step = static_cast<uint32_t>(ph);
       a.num_steps = static_cast<uint32_t>(P);
+      for (const Task& t : rsx.tasks) a.has_nvls |= t.mode == kModeNvlsAllReduce ? 1u : 0u;
       const int resident = plan->ctas_per_sm * rank.sm_count;
       int cap = plan->max_ctas > 0 ? std::min(plan->max_ctas, resident) : resident;
       if (cap <= 0) cap = 148;
@@ -623,7 +672,16 @@ std::string DescribePlan(const Plan& plan) {
           (i < t.nsrc ? src : dst).push_back(ref.slot);
           (i < t.nsrc ? src_region : dst_region).push_back(ref.region);
         }
-        tasks.push_back({{"lo", t.lo}, {"hi", t.hi}, {"vec", t.vec}, {"piece_begin", t.piece_begin},
+        if (t.mode == kModeNvlsAllReduce) {
+          const McGroup* mc = plan.ctx->mc_index[r.ptr_refs[t.ptr_begin].slot];
+          std::vector<int> none;
+          tasks.push_back({{"lo", t.lo}, {"hi", t.hi}, {"vec", t.vec}, {"mode", t.mode},
+                           {"piece_begin", t.piece_begin}, {"src", mc->slots}, {"dst", mc->slots},
+                           {"src_region", std::vector<int>(mc->slots.size(), -1)},
+                           {"dst_region", std::vector<int>(mc->slots.size(), -1)}});
+          continue;
+        }
+        tasks.push_back({{"lo", t.lo}, {"hi", t.hi}, {"vec", t.vec}, {"mode", t.mode}, {"piece_begin", t.piece_begin},
                          {"src", src}, {"dst", dst}, {"src_region", src_region},
                          {"dst_region", dst_region}});
       }

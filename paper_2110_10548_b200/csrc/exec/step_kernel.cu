@@ -173,6 +173,48 @@ __device__ __forceinline__ void VectorChunk(const Task& t, void* const* ptrs, ui
   }
 }
 
+// NVLS AllReduce chunk: the NVSwitch sums the group's copies
+// (multimem.ld_reduce on the multicast address; bf16 accumulates in f32) and
+// multimem.st writes the result to every member. f32 / bf16 only.
+template <int DT, int kUnroll>
+__device__ __forceinline__ void NvlsChunk(const Task& t, void* const* ptrs, uint64_t begin,
+                                          uint64_t end) {
+  char* mc = static_cast<char*>(ptrs[t.ptr_begin]);
+  uint4 v[kUnroll];
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {
+    const uint64_t off = begin + (static_cast<uint64_t>(u) * blockDim.x + threadIdx.x) * 16u;
+    if (off >= end) continue;
+    if constexpr (DT == RS_BF16) {
+      asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                   : "l"(mc + off)
+                   : "memory");
+    } else {
+      asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                   : "l"(mc + off)
+                   : "memory");
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {
+    const uint64_t off = begin + (static_cast<uint64_t>(u) * blockDim.x + threadIdx.x) * 16u;
+    if (off >= end) continue;
+    if constexpr (DT == RS_BF16) {
+      asm volatile("multimem.st.relaxed.sys.global.v4.bf16x2 [%0], {%1, %2, %3, %4};" ::"l"(mc + off),
+                   "r"(v[u].x), "r"(v[u].y), "r"(v[u].z), "r"(v[u].w)
+                   : "memory");
+    } else {
+      asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc + off),
+                   "r"(v[u].x), "r"(v[u].y), "r"(v[u].z), "r"(v[u].w)
+                   : "memory");
+    }
+  }
+}
+
+__device__ __forceinline__ void FenceProxyAlias() { asm volatile("fence.proxy.alias;" ::: "memory"); }
+
 // A scalar task (< 16 bytes): one element per thread.
 template <int DT>
 __device__ void ScalarTask(const Task& t, void* const* ptrs) {
@@ -220,6 +262,7 @@ __global__ void __launch_bounds__(512, kUnroll == 4 ? 2 : 1) StepKernel(const __
     WaitAtLeast(a.inbox + a.wait_ranks[threadIdx.x], base + a.step, a.timeout_ns, a.error_flag);
   }
   __syncthreads();
+  if (a.has_nvls) FenceProxyAlias();
 
   // 3. Pieces, grid-strided; tasks are ordered by piece_begin.
   uint32_t cur = 0;
@@ -230,6 +273,12 @@ __global__ void __launch_bounds__(512, kUnroll == 4 ? 2 : 1) StepKernel(const __
       const uint64_t begin = t.lo + static_cast<uint64_t>(p - t.piece_begin) * a.piece_bytes;
       const uint64_t end = min(t.hi, begin + a.piece_bytes);
       const uint64_t chunk = static_cast<uint64_t>(blockDim.x) * kUnroll * 16u;
+      if constexpr (DT != RS_I32) {
+        if (t.mode == kModeNvlsAllReduce) {
+          for (uint64_t c = begin; c < end; c += chunk) NvlsChunk<DT, kUnroll>(t, a.ptrs, c, min(end, c + chunk));
+          continue;
+        }
+      }
       for (uint64_t c = begin; c < end; c += chunk) VectorChunk<DT, kUnroll>(t, a.ptrs, c, min(end, c + chunk));
     } else {
       ScalarTask<DT>(t, a.ptrs);
@@ -238,6 +287,7 @@ __global__ void __launch_bounds__(512, kUnroll == 4 ? 2 : 1) StepKernel(const __
 
   // 4. Exit: the last CTA to finish publishes the step's epoch to all ranks.
   if (a.nsignal == 0 && a.nfinal == 0) return;
+  if (a.has_nvls) FenceProxyAlias();
   FenceSys();
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -136,7 +136,28 @@ class Context:
         allh = b"".join(gathered)
         nat.check(nat.lib().rs_ctx_open_peers(h, ctypes.c_char_p(allh)))
         dist.barrier(group=group)
-        return cls(h, K, {d: device for d in range(K) if slot_rank[d] == rank}, max_bytes, group=group)
+        ctx = cls(h, K, {d: device for d in range(K) if slot_rank[d] == rank}, max_bytes, group=group)
+
+        # Host all-gather for collective multicast (NVLS) setup during compiles.
+        def _exchange(send, nbytes, recv, _user):
+            try:
+                out = [None] * world
+                dist.all_gather_object(out, ctypes.string_at(send, nbytes), group=group)
+                blob = b"".join(out)
+                ctypes.memmove(recv, blob, len(blob))
+                return 0
+            except Exception:  # pragma: no cover - reported as a status by the library
+                return 1
+
+        ctx._exchange_cb = nat.EXCHANGE_FN(_exchange)
+        nat.check(nat.lib().rs_ctx_set_exchange(h, ctx._exchange_cb, None))
+        return ctx
+
+    @property
+    def nvls(self) -> bool:
+        v = ctypes.c_int(0)
+        nat.check(nat.lib().rs_ctx_nvls(self._h, ctypes.byref(v)))
+        return bool(v.value)
 
     def close(self):
         if self._h:

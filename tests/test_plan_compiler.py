@@ -215,3 +215,31 @@ def test_structural_refusals():
     assert e.value.code == 3
     # an empty program is a valid no-op (RunLowered returns the initial state)
     ctx.compile(LoweredProgram(steps=[]), 8)
+
+
+def test_nvls_plan_structure_virtual():
+    """With NVLS on, AllReduce groups of >= 4 slots on distinct GPUs become
+    multicast tasks (one per owner slice); smaller groups and int32 stay P2P.
+    The plan stays hazard-free (simulated with ordered sums)."""
+    K, progs = golden_programs("cfg2_r01")
+    ctx = executor.Context.virtual(K, list(range(K)), K)
+    ctx.set_option("push_min_bytes", -1)
+    ctx.set_option("nvls", 1)
+    seen = 0
+    for _, _, prog, _ in progs[::10]:
+        for dtype in (numeric.BF16, numeric.I32):
+            plan = ctx.compile(prog, 4099, dtype)
+            desc = plan.describe()
+            for st, (op, groups) in zip(desc["steps"], prog.steps):
+                for rk in st["ranks"]:
+                    for t in rk["tasks"]:
+                        if t.get("mode") == 1:
+                            seen += 1
+                            assert dtype != numeric.I32 and op == 0 and len(t["src"]) >= 4
+            inputs = numeric.synthetic_inputs(K, 4099, dtype)
+            want = [x.copy() for x in inputs]
+            numeric.execute(prog, K, want, dtype, nthreads=1)
+            got = [x.copy() for x in inputs]
+            simulate_plan(desc, got, dtype)
+            assert all(np.array_equal(a.view(np.uint8), b.view(np.uint8)) for a, b in zip(got, want))
+    assert seen > 0
