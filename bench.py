@@ -40,7 +40,10 @@ D_BYTES = 256 << 20
 DTYPE = "bf16"
 ELEMS = D_BYTES // 2
 REQUESTS = [[1], [0, 1]]
+AXES = [2, 4]
 SYSTEM = os.path.join(ROOT, "configs", "b200_sock.json")
+# --workload kN: K = N program devices, one per GPU (BASELINE config 4 descriptors)
+K_DESCRIPTORS = {2: "b200_flat2", 4: "b200_sock4", 8: "b200_sock"}
 
 
 def load_peaks():
@@ -59,12 +62,12 @@ def programs():
     from paper_2110_10548_b200 import planner
     out = []
     for red in REQUESTS:
-        syn = planner.synthesize(SYSTEM, [2, 4], red, payload_bytes=D_BYTES)
+        syn = planner.synthesize(SYSTEM, AXES, red, payload_bytes=D_BYTES)
         for mi, pl in enumerate(syn.placements):
             for pi, prog in enumerate(pl.programs):
                 n = len(pl.partition[0])
                 out.append({"request": red, "matrix": mi, "index": pi, "prog": prog, "group_size": n,
-                            "factors": pl.factors})
+                            "factors": pl.factors, "partition": pl.partition})
     return out
 
 
@@ -202,9 +205,20 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--programs-out", default=None, help="write per-program device times (JSON)")
+    ap.add_argument("--workload", default="config2", choices=["config2", "kN"],
+                    help="config2: BASELINE config 2 (8 slots); kN: K = N slots, one per GPU")
+    ap.add_argument("--no-nvls", action="store_true", help="P2P kernels only (bit-exact everywhere)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    global K_SLOTS, SYSTEM, AXES, REQUESTS
+    if args.workload == "kN":
+        from paper_2110_10548_b200 import planner as _pl
+        K_SLOTS = args.gpus
+        SYSTEM = _pl.config_path(K_DESCRIPTORS[args.gpus])
+        AXES, REQUESTS = [args.gpus], [[0]]
+    if not args.no_nvls:
+        os.environ.setdefault("RS_NVLS", "1")  # used where a group has >= 4 slots on distinct GPUs
 
     import numpy as np
     import torch
@@ -267,6 +281,32 @@ def main():
     barrier()
     prog_us = [a.elapsed_time(b) * 1e3 for a, b in ev]
 
+    # NCCL's default AllReduce on the same bytes, one communicator per
+    # reduction group (ReductionGroupPartition), all groups concurrently.
+    nccl_us = {}
+    if multi and world == K_SLOTS:
+        xbuf = torch.randn(ELEMS, device=dev).to(torch.bfloat16)
+        parts = {}
+        for e in entries:
+            parts.setdefault((tuple(e["request"]), e["matrix"]), e["partition"])
+        for key, part in parts.items():
+            groups = [dist.new_group(ranks=g) for g in part]
+            mine = next(grp for grp, g in zip(groups, part) if rank in g)
+            for _ in range(3):
+                dist.all_reduce(xbuf, group=mine)
+            barrier()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(5):
+                dist.all_reduce(xbuf, group=mine)
+            b.record(stream)
+            barrier()
+            t = torch.tensor([a.elapsed_time(b) * 1e3 / 5], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            nccl_us[key] = float(t.item())
+        del xbuf
+
     sampler = ClockSampler(local_rank) if rank == 0 else None
     if sampler:
         sampler.start()
@@ -328,7 +368,13 @@ def main():
             inst["allreduce_us"] = round(us, 2)
         if us < inst["best_us"]:
             inst["best_us"], inst["best"] = round(us, 2), e["prog"].text
+    for key, inst in instances.items():
+        if key in nccl_us:
+            inst["nccl_allreduce_us"] = round(nccl_us[key], 2)
+            inst["speedup_vs_nccl"] = round(nccl_us[key] / inst["best_us"], 4)
     inst_list = list(instances.values())
+    speedups = [i["speedup_vs_nccl"] for i in inst_list if "speedup_vs_nccl" in i]
+    speedup_vs_nccl = round(float(statistics.geometric_mean(speedups)), 4) if speedups else None
     from paper_2110_10548_b200 import rescore
     resc = rescore.topk([{"instance": (tuple(e["request"]), e["matrix"]), "index": e["index"],
                           "sim_seconds": e["prog"].seconds, "measured_us": us, "text": e["prog"].text}
@@ -379,8 +425,10 @@ def main():
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "config 2: all 754 synthesized programs (axes [2,4] on b200_sock, reduce {1} "
-                                   "and {0,1}), 8 slots x 256 MiB bf16",
+            "config": {"workload": ("config 2: all 754 synthesized programs (axes [2,4] on b200_sock, reduce {1} "
+                                    "and {0,1}), 8 slots x 256 MiB bf16") if args.workload == "config2" else
+                                   (f"config 4 K={K_SLOTS}: all {len(entries)} programs of "
+                                    f"{os.path.basename(SYSTEM)} axes {AXES}, {K_SLOTS} slots x 256 MiB bf16"),
                        "slots_per_gpu": K_SLOTS // world, "programs": len(entries),
                        "parallelism": f"{world} GPU(s), slots block-distributed",
                        "l2": "inputs larger than L2 (8 x 256 MiB)"},
@@ -393,6 +441,8 @@ def main():
                            "max": round(max(prog_us), 2)},
             "instances": inst_list,
             "simulator_rescoring": sim_topk,
+            "speedup_vs_nccl": speedup_vs_nccl,
+            "nvls": bool(getattr(ctx, "nvls", False)) if world > 1 else False,
         }
         print(json.dumps(line), flush=True)
     barrier()

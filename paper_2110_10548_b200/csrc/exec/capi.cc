@@ -178,8 +178,10 @@ int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value) {
   } else if (k == "nvls_min_group") {
     if (value < 2) return Bad("nvls_min_group must be >= 2");
     ctx->impl->nvls_min_group = static_cast<int>(value);
+  } else if (k == "nvls_min_bytes") {
+    ctx->impl->nvls_min_bytes = value < 0 ? ~0ull : static_cast<uint64_t>(value);
   } else {
-    return Bad("unknown option (push_min_bytes | barrier_timeout_ms | nvls | nvls_min_group)");
+    return Bad("unknown option (push_min_bytes | barrier_timeout_ms | nvls | nvls_min_group | nvls_min_bytes)");
   }
   return RS_OK;
 }

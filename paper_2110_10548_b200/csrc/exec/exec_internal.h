@@ -58,6 +58,7 @@ typedef int (*ExchangeFn)(const void* send, size_t bytes, void* recv, void* user
 // A pointer-table entry: slot `slot`'s buffer (region -1) or its scratch
 // region `region`.
 constexpr int kMcRegion = -2;  // Ref{mc group index, kMcRegion}: a multicast base
+constexpr size_t kMaxMcGroups = 32;  // multicast objects per context (switch resources)
 
 struct Ref {
   int slot;    // slot id, or mc group index for kMcRegion
@@ -92,6 +93,9 @@ class Context {
   bool use_vmm = false;
   bool nvls = false;
   int nvls_min_group = 4;
+  // Below this many bytes per group the P2P kernel's lower latency wins
+  // (measured crossover ~16 MiB at n = 4, profiles/r01_sweep_n4_bf16_graph_nvls.json).
+  uint64_t nvls_min_bytes = 16ull << 20;
   ExchangeFn exchange = nullptr;  // host all-gather (multi-process NVLS setup)
   void* exchange_user = nullptr;
   std::map<std::vector<int>, std::unique_ptr<McGroup>> mc_groups;

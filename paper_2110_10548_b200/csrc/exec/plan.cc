@@ -228,8 +228,9 @@ struct Compiler {
   // NVLS applies to AllReduce groups of >= nvls_min_group slots, one per GPU,
   // for floating-point data.
   bool NvlsEligible(const std::vector<int>& g, uint64_t bytes) const {
-    if (!ctx->nvls || dtype == RS_I32 || bytes == 0) return false;
+    if (!ctx->nvls || dtype == RS_I32 || bytes == 0 || bytes < ctx->nvls_min_bytes) return false;
     if (static_cast<int>(g.size()) < ctx->nvls_min_group) return false;
+    if (ctx->mc_groups.size() >= kMaxMcGroups && !ctx->mc_groups.count(g)) return false;
     std::vector<int> ranks;
     for (int d : g) ranks.push_back(ctx->slot_rank[d]);
     std::sort(ranks.begin(), ranks.end());
@@ -248,10 +249,14 @@ struct Compiler {
         for (int i = 0; i < n; ++i) owners[i] = i;
         std::vector<Ref> all;
         for (int m : g) all.push_back(Buf(m));
-        if (NvlsEligible(g, TotalBytes(ranges))) {
-          int mc = -1;
-          absl::Status s = EnsureMulticast(ctx, g, &mc);
-          if (!s.ok()) return s;
+        int mc = -1;
+        if (NvlsEligible(g, TotalBytes(ranges)) && !EnsureMulticast(ctx, g, &mc).ok()) {
+          // Every rank sees the same failure (the setup exchanges carry each
+          // rank's status), so all fall back to P2P consistently.
+          ctx->nvls = false;
+          mc = -1;
+        }
+        if (mc >= 0) {
           const std::vector<std::vector<Range>> parts = SplitEven(ranges, n);
           for (int p = 0; p < n; ++p)
             for (const Range& r : parts[p]) out.b.push_back(ProtoTask{g[p], r, all, all, mc});

@@ -86,6 +86,7 @@ def nvls_ctx():
         pytest.skip("multicast not supported")
     if n == 2:
         ctx.set_option("nvls_min_group", 2)
+    ctx.set_option("nvls_min_bytes", 0)  # exercise NVLS at every size
     yield ctx, n
     ctx.close()
 
@@ -156,6 +157,7 @@ def _mp_worker(rank, world, port, result_dir):
         assert ctx.nvls, "NVLS not enabled"
         if world == 2:
             ctx.set_option("nvls_min_group", 2)
+        ctx.set_option("nvls_min_bytes", 0)
         used = 0
         for dt in (numeric.BF16, numeric.F32):
             for N in (5003, 4 << 20):

@@ -225,6 +225,7 @@ def test_nvls_plan_structure_virtual():
     ctx = executor.Context.virtual(K, list(range(K)), K)
     ctx.set_option("push_min_bytes", -1)
     ctx.set_option("nvls", 1)
+    ctx.set_option("nvls_min_bytes", 0)
     seen = 0
     for _, _, prog, _ in progs[::10]:
         for dtype in (numeric.BF16, numeric.I32):
