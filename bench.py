@@ -13,9 +13,10 @@ per GPU, every step over NVLink/NVSwitch). Total work is fixed as N grows
 value = aggregate bus bandwidth of the step = sum over programs of
 K * D * 2(n-1)/n (nccl-tests AllReduce bus bytes, n = reduction-group size,
 D = 256 MiB) divided by the device-timed step (max over ranks).
-e2e   = the same metric through the C-ABI from pinned HOST buffers (H2D
-copy-in + program + D2H copy-out inside the timed region) on a fixed
-8-program sample of the same set.
+e2e   = the same metric through the C-ABI from pinned HOST buffers: each
+step uploads the 8 input buffers (rs_ctx_upload, 2 GiB), runs all programs
+(rs_plan_run) and downloads the 8 results (rs_ctx_download, 2 GiB), all
+inside the timed region.
 
 Usage: python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 For N>1 launch under torchrun (one rank per GPU, NCCL process group).
@@ -382,35 +383,40 @@ def main():
                          for e, us in zip(entries, prog_us)])
     sim_topk = {"instances": resc["instances"], "top_k": resc["top_k"], "top_k_tie_aware": resc["top_k_tie_aware"]}
 
-    # end to end from pinned host memory (fixed sample)
+    # End to end through the C-ABI from pinned HOST memory: every step
+    # uploads the hosted slots' inputs (rs_ctx_upload), runs the step's
+    # programs (rs_plan_run), and downloads the results (rs_ctx_download).
     e2e = None
     if not args.no_e2e:
-        sample_idx = list(range(0, len(plans), max(1, len(plans) // 8)))[:8]
-        host = {}
-        for d in ctx.hosted_slots:
-            host[d] = ctx.buffer(d, ELEMS, "bf16").cpu().pin_memory()
-        hb = [host.get(d) for d in range(K_SLOTS)]
+        host_in = {d: ctx.buffer(d, ELEMS, "bf16").cpu().pin_memory() for d in ctx.hosted_slots}
+        host_out = {d: torch.empty_like(t).pin_memory() for d, t in host_in.items()}
+        e2e_steps = max(1, min(args.steps, 2))
         barrier()
         h0 = time.perf_counter()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for i in sample_idx:
-            plans[i].run_host(hb)
+        for _ in range(e2e_steps):
+            for d, t in host_in.items():
+                ctx.upload(d, t)
+            step()
+            for d, t in host_out.items():
+                ctx.download(d, t)
         e1.record(stream)
         barrier()
-        e2e_ms = e0.elapsed_time(e1)
+        e2e_ms = e0.elapsed_time(e1) / e2e_steps
         if multi:
             t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
-        wall_ms = (time.perf_counter() - h0) * 1e3
-        nbytes = len(ctx.hosted_slots) * D_BYTES * len(sample_idx)
-        e2e = {"value": round(sum(bus_bytes(entries[i]) for i in sample_idx) / (e2e_ms * 1e-3) / 1e9, 3),
+        wall_ms = (time.perf_counter() - h0) * 1e3 / e2e_steps
+        nbytes = K_SLOTS * D_BYTES
+        e2e = {"value": round(bus_per_step / (e2e_ms * 1e-3) / 1e9, 3),
                "unit": "GB/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-               "sample": f"{len(sample_idx)} programs (every {max(1, len(plans) // 8)}th), host buffers pinned",
-               "ms": round(e2e_ms, 2), "wall_ms": round(wall_ms, 2)}
-        del host, hb
+               "sample": f"full step ({len(plans)} programs) between an H2D of the {K_SLOTS} input buffers "
+                         f"and a D2H of the results, pinned host memory, {e2e_steps} step(s)",
+               "ms_per_step": round(e2e_ms, 2), "wall_ms_per_step": round(wall_ms, 2)}
+        del host_in, host_out
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -87,6 +87,12 @@ int rs_ctx_destroy(rs_ctx* ctx);
  * process only). Programs run in place on these buffers when rs_plan_run is
  * given no user buffers. */
 int rs_ctx_buffer(rs_ctx* ctx, int slot, void** device_ptr);
+/* Copy `bytes` between host memory (pinned for speed) and the start of slot
+ * d's buffer (hosted slots only), asynchronously on `stream` (NULL = the
+ * context's stream of that slot's GPU). Used to stage inputs once and run
+ * several plans in place before reading the results back. */
+int rs_ctx_upload(rs_ctx* ctx, int slot, const void* host, size_t bytes, void* stream);
+int rs_ctx_download(rs_ctx* ctx, int slot, void* host, size_t bytes, void* stream);
 /* Number of ranks driven by this process and their CUDA ordinals. */
 int rs_ctx_local_ranks(rs_ctx* ctx, int* count, int* ordinals /* RS_MAX_RANKS */);
 /* Context knobs applied to plans compiled afterwards: "push_min_bytes"

@@ -29,7 +29,7 @@ EXPORTED_SYMBOLS = (
     "rs_last_error", "rs_version",
     "rs_ctx_create", "rs_ctx_create_rank", "rs_ctx_ipc_handle", "rs_ctx_open_peers",
     "rs_ctx_create_virtual", "rs_plan_describe_json", "rs_ctx_set_option", "rs_ctx_nvls",
-    "rs_ctx_set_exchange",
+    "rs_ctx_set_exchange", "rs_ctx_upload", "rs_ctx_download",
     "rs_ctx_destroy", "rs_ctx_buffer", "rs_ctx_local_ranks", "rs_ctx_synchronize",
     "rs_plan_compile", "rs_plan_run", "rs_plan_run_host", "rs_plan_launch_count",
     "rs_plan_step_bytes", "rs_plan_set_launch", "rs_plan_set_option", "rs_plan_destroy",
@@ -75,6 +75,8 @@ def _declare(lib):
         "rs_plan_describe_json": (_I, [_P, ctypes.POINTER(ctypes.c_void_p)]),
         "rs_ctx_set_option": (_I, [_P, ctypes.c_char_p, ctypes.c_longlong]),
         "rs_ctx_nvls": (_I, [_P, _PI]),
+        "rs_ctx_upload": (_I, [_P, _I, _P, _SZ, _P]),
+        "rs_ctx_download": (_I, [_P, _I, _P, _SZ, _P]),
         "rs_ctx_set_exchange": (_I, [_P, EXCHANGE_FN, _P]),
         "rs_ctx_open_peers": (_I, [_P, _P]),
         "rs_ctx_destroy": (_I, [_P]),

@@ -101,6 +101,30 @@ int rs_ctx_buffer(rs_ctx* ctx, int slot, void** device_ptr) {
   return RS_OK;
 }
 
+static int CopySlot(rs_ctx* ctx, int slot, void* host, size_t bytes, void* stream, bool up) {
+  if (!ctx || !host) return Bad("null argument");
+  rs::Context* c = ctx->impl;
+  if (slot < 0 || slot >= c->K) return Bad("slot out of range");
+  const int r = c->slot_rank[slot];
+  if (!c->ranks[r].driven) return Bad("slot is not hosted by this process");
+  if (bytes > c->max_bytes) return Bad("copy larger than max_bytes");
+  absl::Status s = rs::CudaStatus(cudaSetDevice(c->ranks[r].ordinal), "cudaSetDevice");
+  if (!s.ok()) return Report(s);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->ranks[r].stream;
+  void* dev = c->SlotPtr(r, slot);
+  return Report(rs::CudaStatus(up ? cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, st)
+                                  : cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, st),
+                               up ? "upload" : "download"));
+}
+
+int rs_ctx_upload(rs_ctx* ctx, int slot, const void* host, size_t bytes, void* stream) {
+  return CopySlot(ctx, slot, const_cast<void*>(host), bytes, stream, true);
+}
+
+int rs_ctx_download(rs_ctx* ctx, int slot, void* host, size_t bytes, void* stream) {
+  return CopySlot(ctx, slot, host, bytes, stream, false);
+}
+
 int rs_ctx_local_ranks(rs_ctx* ctx, int* count, int* ordinals) {
   if (!ctx || !count) return Bad("null argument");
   const std::vector<int> driven = ctx->impl->DrivenRanks();

@@ -198,6 +198,30 @@ class Context:
     def read(self, slot: int, nbytes: int) -> np.ndarray:
         return self.buffer_bytes(slot, nbytes).cpu().numpy()
 
+    def _host(self, buf):
+        if isinstance(buf, np.ndarray):
+            return buf.ctypes.data, buf.nbytes
+        return buf.data_ptr(), buf.numel() * buf.element_size()
+
+    def _stream_of(self, slot, stream):
+        if stream is not None:
+            return stream
+        import torch
+        return torch.cuda.current_stream(self.slot_ordinal[slot]).cuda_stream
+
+    def upload(self, slot: int, host, stream=None):
+        """Async H2D copy (C-ABI rs_ctx_upload) of a host buffer (pinned
+        torch tensor or numpy array) into slot `slot`."""
+        ptr, n = self._host(host)
+        nat.check(nat.lib().rs_ctx_upload(self._h, slot, ctypes.c_void_p(ptr), n,
+                                          ctypes.c_void_p(self._stream_of(slot, stream))))
+
+    def download(self, slot: int, host, stream=None):
+        """Async D2H copy (C-ABI rs_ctx_download) of slot `slot` into `host`."""
+        ptr, n = self._host(host)
+        nat.check(nat.lib().rs_ctx_download(self._h, slot, ctypes.c_void_p(ptr), n,
+                                            ctypes.c_void_p(self._stream_of(slot, stream))))
+
     @property
     def hosted_slots(self):
         return sorted(self.slot_ordinal)
