@@ -87,6 +87,17 @@ def device_tensor(ptr: int, numel: int, dtype_name: str, device_id: int):
 
 # ---- context / plan ---------------------------------------------------------
 
+_CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
+
+
+def _stream_handle(stream) -> int:
+    """torch stream -> cudaStream_t for the C-ABI. torch's default stream is
+    the legacy NULL stream; pass it explicitly as cudaStreamLegacy because the
+    C-ABI reads NULL as "the context's own stream"."""
+    h = stream.cuda_stream
+    return h if h else _CUDA_STREAM_LEGACY
+
+
 class Context:
     """Owns the per-GPU heaps (slot buffers + barrier flags) of K slots."""
 
@@ -207,7 +218,7 @@ class Context:
         if stream is not None:
             return stream
         import torch
-        return torch.cuda.current_stream(self.slot_ordinal[slot]).cuda_stream
+        return _stream_handle(torch.cuda.current_stream(self.slot_ordinal[slot]))
 
     def upload(self, slot: int, host, stream=None):
         """Async H2D copy (C-ABI rs_ctx_upload) of a host buffer (pinned
@@ -272,7 +283,7 @@ class Plan:
     def _streams(self, streams):
         if streams is None:
             import torch
-            streams = [torch.cuda.current_stream(o).cuda_stream for o in self.ctx.local_ordinals]
+            streams = [_stream_handle(torch.cuda.current_stream(o)) for o in self.ctx.local_ordinals]
         arr = (ctypes.c_void_p * max(1, len(streams)))(*[ctypes.c_void_p(s) for s in streams])
         return arr
 

@@ -156,6 +156,32 @@ def test_user_and_host_buffer_paths(local8):
         assert np.array_equal(host[d].numpy(), want[d])
 
 
+def test_upload_run_download_stream_ordered(local8):
+    """rs_ctx_upload -> several plans in place -> rs_ctx_download, all async on
+    torch's current stream: results equal the oracle applied in sequence."""
+    K, progs = golden_programs("cfg2_r01")
+    N = 1 << 20
+    inputs = numeric.synthetic_inputs(K, N, numeric.I32)
+    host_in = [torch.from_numpy(x.copy()).pin_memory() for x in inputs]
+    host_out = [torch.empty_like(t).pin_memory() for t in host_in]
+    chain = [progs[i][2] for i in (0, 77, 311)]
+    plans = [local8.compile(p, N, "i32") for p in chain]
+    for d in range(K):
+        local8.upload(d, host_in[d])
+    for p in plans:
+        p.run()
+    for d in range(K):
+        local8.download(d, host_out[d])
+    torch.cuda.current_stream().synchronize()
+    want = [x.copy() for x in inputs]
+    for p in chain:
+        numeric.execute(p, K, want, numeric.I32)
+    for d in range(K):
+        assert np.array_equal(host_out[d].numpy(), want[d])
+    for p in plans:
+        p.close()
+
+
 def test_refusal_launches_nothing(local8):
     from paper_2110_10548_b200.planner import LoweredProgram
     bad = LoweredProgram(steps=[(3, [[0, 1, 2, 3]]), (3, [[0, 1, 2, 3]])])
