@@ -3,7 +3,7 @@
 device per GPU), every synthesized program of the K-GPU descriptor against
 NCCL's default AllReduce on the same bytes.
 
-  torchrun --nproc-per-node N bench_sweep.py [--dtype bf16] [--min 1024]
+  torchrun --nproc-per-node N bench_sweep.py [--dtype bf16] [--min-bytes 1024]
            [--max 1073741824] [--iters 20] [--out profiles/sweep_nN.json]
 
 Descriptors: K=2 [(node,1),(gpu,2)]; K=4 [(node,1),(socket,2),(gpu,2)];
@@ -28,8 +28,8 @@ DESCRIPTORS = {2: "b200_flat2", 4: "b200_sock4", 8: "b200_sock"}
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
-    ap.add_argument("--min", type=int, default=1 << 10)
-    ap.add_argument("--max", type=int, default=1 << 30)
+    ap.add_argument("--min-bytes", dest="min", type=int, default=1 << 10)
+    ap.add_argument("--max-bytes", dest="max", type=int, default=1 << 30)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--programs", default="all", help="'all' or 'first:N'")

@@ -118,6 +118,7 @@ struct RankStep {
   std::vector<Task> tasks;
   std::vector<Ref> ptr_refs;  // pointer-table entries
   uint32_t npieces = 0;
+  uint32_t piece_bytes = kPieceBytes;  // 4 KiB .. 64 KiB, sized to fill the GPU
   std::vector<uint8_t> wait;  // ranks to wait for before the phase
   double tx_bytes = 0, rx_bytes = 0, hbm_bytes = 0;
 };

@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <map>
 #include <memory>
+#include <cstdlib>
 #include <set>
 
 #include "absl/strings/str_format.h"
@@ -484,6 +485,16 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
   plan->dtype = dtype;
   plan->elems = elems;
   plan->bytes = elems * es;
+  // Launch-shape defaults (tuning / A-B runs): RS_THREADS, RS_UNROLL, RS_MAX_CTAS.
+  if (const char* v = std::getenv("RS_THREADS")) {
+    const int t = std::atoi(v);
+    if (t >= 32 && t <= 512 && t % 32 == 0) plan->threads = t;
+  }
+  if (const char* v = std::getenv("RS_UNROLL")) {
+    const int u = std::atoi(v);
+    if (u == 4 || u == 8) plan->unroll = u;
+  }
+  if (const char* v = std::getenv("RS_MAX_CTAS")) plan->max_ctas = std::max(0, std::atoi(v));
 
   // 2./3. Tasks per step, laid out into one or two phases.
   Compiler comp(ctx, elems, es, dtype);
@@ -501,9 +512,19 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
       if (list == &tasks.a && list->empty()) continue;
       plan->phases.emplace_back(R);
       plan->phase_step.push_back(s);
+      // Piece size per rank: enough pieces to occupy ~2 CTAs per SM (memory
+      // parallelism for remote loads), between 4 KiB and kPieceBytes.
+      std::vector<uint64_t> rank_bytes(R, 0);
+      for (const ProtoTask& t : *list) rank_bytes[ctx->slot_rank[t.owner]] += t.range.hi - t.range.lo;
+      for (int r = 0; r < R; ++r) {
+        uint32_t pb = 4u << 10;
+        while (pb < kPieceBytes && rank_bytes[r] / pb > 2 * 148) pb <<= 1;
+        plan->phases.back()[r].piece_bytes = pb;
+      }
       for (const ProtoTask& t : *list) {
         AddTraffic(plan->phases.back(), *ctx, t);
-        Lay(plan->phases.back()[ctx->slot_rank[t.owner]], t, kPieceBytes);
+        RankStep& rs = plan->phases.back()[ctx->slot_rank[t.owner]];
+        Lay(rs, t, rs.piece_bytes);
       }
     }
   }
@@ -621,7 +642,7 @@ absl::Status RunPlan(Plan* plan, void* const* device_bufs, void* const* host_buf
       a.ptrs = plan->d_ptrs[r] ? plan->d_ptrs[r] + plan->ptr_offset[r][ph] : nullptr;
       a.ntasks = static_cast<uint32_t>(rsx.tasks.size());
       a.npieces = rsx.npieces;
-      a.piece_bytes = kPieceBytes;
+      a.piece_bytes = rsx.piece_bytes;
       a.dtype = plan->dtype;
       a.arrive_counter = reinterpret_cast<unsigned int*>(rank.heap + kCounterOffset);
       a.error_flag = reinterpret_cast<int*>(rank.heap + kErrorOffset);

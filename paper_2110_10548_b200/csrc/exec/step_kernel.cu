@@ -61,14 +61,17 @@ __device__ __forceinline__ uint64_t GlobalTimer() {
 // (the data is then wrong, but the GPU is not hung; the host reports it).
 __device__ void WaitAtLeast(const uint64_t* flag, uint64_t target, uint64_t timeout_ns,
                             int* error_flag) {
-  if (LoadAcquireSys(flag) >= target) return;
+  // Tight spin first (a peer is usually < 2 us away), then back off.
+  for (int i = 0; i < 4096; ++i) {
+    if (LoadAcquireSys(flag) >= target) return;
+  }
   const uint64_t t0 = GlobalTimer();
   while (LoadAcquireSys(flag) < target) {
     if (GlobalTimer() - t0 > timeout_ns) {
       atomicExch(error_flag, 1);
       return;
     }
-    __nanosleep(32);
+    __nanosleep(64);
   }
 }
 
@@ -287,13 +290,15 @@ __global__ void __launch_bounds__(512, kUnroll == 4 ? 2 : 1) StepKernel(const __
 
   // 4. Exit: the last CTA to finish publishes the step's epoch to all ranks.
   if (a.nsignal == 0 && a.nfinal == 0) return;
-  if (a.has_nvls) FenceProxyAlias();
-  FenceSys();
+  // The CTA barrier orders every thread's stores before thread 0's system
+  // fence (cumulativity); one fence per CTA instead of one per thread.
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned prev = atomicAdd(a.arrive_counter, 1u);
-    if (prev == gridDim.x - 1) {
-      atomicExch(a.arrive_counter, 0u);
+    if (a.has_nvls) FenceProxyAlias();
+    FenceSys();
+    const bool last = gridDim.x == 1 || atomicAdd(a.arrive_counter, 1u) == gridDim.x - 1;
+    if (last) {
+      if (gridDim.x > 1) atomicExch(a.arrive_counter, 0u);
       FenceSys();
       for (uint32_t q = 0; q < a.nsignal; ++q) StoreReleaseSys(a.signal_ptrs[q], base + a.step + 1);
       // 5. Last step: the run is complete here only once every rank that
