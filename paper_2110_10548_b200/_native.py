@@ -12,7 +12,7 @@ import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(_HERE, "_lib")
-LIB_PATH = os.path.join(LIB_DIR, "libredsynth_b200.so")
+LIB_PATH = os.environ.get("RS_LIB_PATH") or os.path.join(LIB_DIR, "libredsynth_b200.so")
 
 RS_OK = 0
 RS_INVALID_ARGUMENT = 3

@@ -485,6 +485,9 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
   plan->dtype = dtype;
   plan->elems = elems;
   plan->bytes = elems * es;
+  // One GPU (HBM-bound): 8 vectors in flight per thread per source measured
+  // +1.7% over 4; across GPUs 4 is as good or better (profiles/r01_tune_*).
+  if (ctx->world == 1) plan->unroll = 8;
   // Launch-shape defaults (tuning / A-B runs): RS_THREADS, RS_UNROLL, RS_MAX_CTAS.
   if (const char* v = std::getenv("RS_THREADS")) {
     const int t = std::atoi(v);
