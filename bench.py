@@ -344,10 +344,19 @@ def main():
                 alg += p.step_bytes(s)[1]  # local mode: minimal HBM bytes of the tasks
         peak, peak_kind = load_peaks()
         achieved = alg / (ms_per_step * 1e-3) / 1e9
+        traffic, tnote = None, "no ncu capture found"
+        try:  # committed ncu --set full capture of the same kernel (profiles/)
+            with open(os.path.join(ROOT, "profiles", "r01b_ncu_local.json")) as f:
+                cap = json.load(f)["launches"][0]
+            traffic = cap["dram_bytes"]
+            tnote = (f"traffic = dram read+write bytes of one profiled launch ({cap['what']}), "
+                     f"{cap['dram_bytes'] / cap['algorithmic_bytes']:.3f} x its algorithmic bytes")
+        except Exception:
+            pass
         roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(achieved / peak, 4), "traffic": None,
+                    "frac": round(achieved / peak, 4), "traffic": traffic,
                     "note": f"algorithmic bytes = sum over tasks of (sources + destinations) x range "
-                            f"(minimal HBM traffic), per step {alg / 1e9:.2f} GB; peak {peak_kind}"}
+                            f"(minimal HBM traffic), per step {alg / 1e9:.2f} GB; peak {peak_kind}; {tnote}"}
     else:
         if world == K_SLOTS:
             alg = sum(algorithmic_link_bytes(e["prog"], K_SLOTS, D_BYTES) for e in entries)
