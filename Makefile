@@ -26,9 +26,9 @@ EXEC_OBJS    := $(patsubst $(PKG)/csrc/exec/%.cc,$(LIB)/obj/exec_%.o,$(EXEC_CC))
                 $(patsubst $(PKG)/csrc/exec/%.cu,$(LIB)/obj/cu_%.o,$(EXEC_CU))
 
 .PHONY: all planner exec oracle check-ref clean
-all: planner exec $(LIB)/execute_example
+all: planner exec $(LIB)/synth $(LIB)/execute_example
 
-planner: $(LIB)/libredsynth_planner.a $(LIB)/synth
+planner: $(LIB)/libredsynth_planner.a
 
 $(LIB)/obj/%.o: $(PKG)/csrc/planner/%.cc $(wildcard include/redsynth/*.h)
 	@mkdir -p $(LIB)/obj
@@ -37,8 +37,9 @@ $(LIB)/obj/%.o: $(PKG)/csrc/planner/%.cc $(wildcard include/redsynth/*.h)
 $(LIB)/libredsynth_planner.a: $(PLANNER_OBJS)
 	ar rcs $@ $^
 
-$(LIB)/synth: $(PKG)/csrc/tools/synth_main.cc $(LIB)/libredsynth_planner.a
-	$(CXX) $(CXXFLAGS) $(INC) -o $@ $< $(LIB)/libredsynth_planner.a -pthread
+# The CLI links the executor library (planner + C-ABI; no libcuda dependency).
+$(LIB)/synth: $(PKG)/csrc/tools/synth_main.cc $(LIB)/libredsynth_b200.so
+	$(CXX) $(CXXFLAGS) $(INC) $(CUDA_INC) -o $@ $< -L$(LIB) -lredsynth_b200 -Wl,-rpath,'$$ORIGIN' -pthread
 
 exec: $(LIB)/libredsynth_b200.so
 
@@ -59,7 +60,7 @@ $(LIB)/execute_example: examples/execute_program.cc $(LIB)/libredsynth_b200.so
 oracle:
 	$(MAKE) -C oracle numeric ref
 
-check-ref: planner
+check-ref: all
 	$(MAKE) -C oracle mine-tests
 
 clean:

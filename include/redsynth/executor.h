@@ -41,6 +41,9 @@ class CompiledProgram {
   // Copies K device buffers (slot-indexed) in, runs, copies them back out.
   absl::Status Run(std::span<void* const> device_buffers);
   int launches_per_run() const;
+  // Device time of one run in microseconds (warmup untimed runs, then iters
+  // timed back-to-back runs; slowest GPU). Synchronous.
+  absl::StatusOr<double> TimeUs(int warmup = 1, int iters = 5);
 
  private:
   friend class GpuExecutor;

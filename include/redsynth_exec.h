@@ -144,6 +144,11 @@ int rs_plan_run(rs_plan* plan, void* const* device_bufs, void* const* streams);
  * result back (D2H). Async on the given/own streams. */
 int rs_plan_run_host(rs_plan* plan, void* const* host_bufs, void* const* streams);
 
+/* Device time of one run: `warmup` untimed runs, then `iters` back-to-back
+ * runs bracketed by CUDA events on every local rank's stream; *us = the
+ * slowest rank's elapsed time / iters. Synchronous. */
+int rs_plan_time(rs_plan* plan, int warmup, int iters, double* us);
+
 /* Kernel launches one rs_plan_run performs (all local ranks). */
 int rs_plan_launch_count(rs_plan* plan, int* launches);
 

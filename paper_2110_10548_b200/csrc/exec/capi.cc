@@ -160,6 +160,42 @@ int rs_plan_run_host(rs_plan* plan, void* const* host_bufs, void* const* streams
   return Report(rs::RunPlan(plan->impl, nullptr, host_bufs, streams));
 }
 
+int rs_plan_time(rs_plan* plan, int warmup, int iters, double* us) {
+  if (!plan || !us || iters < 1 || warmup < 0) return Bad("bad argument");
+  rs::Plan* p = plan->impl;
+  const std::vector<int> driven = p->ctx->DrivenRanks();
+  for (int i = 0; i < warmup; ++i) {
+    absl::Status s = rs::RunPlan(p, nullptr, nullptr, nullptr);
+    if (!s.ok()) return Report(s);
+  }
+  std::vector<cudaEvent_t> e0(driven.size()), e1(driven.size());
+  for (size_t i = 0; i < driven.size(); ++i) {
+    const rs::Rank& rk = p->ctx->ranks[driven[i]];
+    cudaSetDevice(rk.ordinal);
+    cudaEventCreate(&e0[i]);
+    cudaEventCreate(&e1[i]);
+    cudaEventRecord(e0[i], rk.stream);
+  }
+  for (int i = 0; i < iters; ++i) {
+    absl::Status s = rs::RunPlan(p, nullptr, nullptr, nullptr);
+    if (!s.ok()) return Report(s);
+  }
+  float worst = 0.f;
+  for (size_t i = 0; i < driven.size(); ++i) {
+    const rs::Rank& rk = p->ctx->ranks[driven[i]];
+    cudaSetDevice(rk.ordinal);
+    cudaEventRecord(e1[i], rk.stream);
+    cudaEventSynchronize(e1[i]);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0[i], e1[i]);
+    worst = std::max(worst, ms);
+    cudaEventDestroy(e0[i]);
+    cudaEventDestroy(e1[i]);
+  }
+  *us = 1e3 * worst / iters;
+  return Report(rs::Synchronize(p->ctx));
+}
+
 int rs_plan_launch_count(rs_plan* plan, int* launches) {
   if (!plan || !launches) return Bad("null argument");
   *launches = plan->impl->num_phases() * static_cast<int>(plan->impl->ctx->DrivenRanks().size());

@@ -46,6 +46,13 @@ absl::Status CompiledProgram::Run(std::span<void* const> device_buffers) {
   return FromCode(rs_plan_run(plan_, device_buffers.data(), nullptr));
 }
 
+absl::StatusOr<double> CompiledProgram::TimeUs(int warmup, int iters) {
+  double us = 0;
+  absl::Status s = FromCode(rs_plan_time(plan_, warmup, iters, &us));
+  if (!s.ok()) return s;
+  return us;
+}
+
 int CompiledProgram::launches_per_run() const {
   int n = 0;
   rs_plan_launch_count(plan_, &n);

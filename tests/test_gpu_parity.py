@@ -253,3 +253,24 @@ def test_cpp_host_example_end_to_end():
     assert r.returncode == 0, r.stdout + r.stderr
     assert "programs=500 mismatches=0" in r.stdout
     assert "step 1: Reduce over devices {0,1}: devices hold different chunk sets" in r.stdout
+
+
+def test_synth_cli_execute_mode(tmp_path):
+    """`synth --execute`: the reference report plus measured columns."""
+    import json
+    import subprocess
+    from common import ROOT
+    exe = os.path.join(ROOT, "paper_2110_10548_b200", "_lib", "synth")
+    out = tmp_path / "r.json"
+    r = subprocess.run([exe, "--system", os.path.join(ROOT, "configs", "b200_sock.json"), "--axes", "2,4",
+                        "--reduce", "0", "--bytes", str(8 << 20), "--execute", "--iters", "3", "--out", str(out)],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    doc = json.loads(out.read_text())
+    assert doc["executed"]["dtype"] == "bf16"
+    for m in doc["matrices"]:
+        assert m["measured_best"]["us"] > 0
+        ranks = sorted(p["measured_rank"] for p in m["programs"])
+        assert ranks == list(range(1, len(m["programs"]) + 1))
+        for p in m["programs"]:
+            assert p["measured_us"] > 0 and p["bus_GBps"] > 0
