@@ -100,7 +100,13 @@ int rs_ctx_local_ranks(rs_ctx* ctx, int* count, int* ordinals /* RS_MAX_RANKS */
  * store-only variant; -1 disables it; default disabled, env RS_PUSH_MIN_BYTES)
  * and "barrier_timeout_ms" (device-side spin limit, default 20 s). Scratch
  * for the push variant is reserved at creation: min(K, 8) buffers per slot on
- * multi-GPU contexts (env RS_SCRATCH_REGIONS). */
+ * multi-GPU contexts (env RS_SCRATCH_REGIONS). "ll_max_bytes": a step whose
+ * cross-GPU groups have one member per GPU and in which no GPU sends a peer
+ * more than this many bytes runs one-shot (LL): sources are pushed as flagged
+ * 16-byte packets into each receiver's LL area and every destination sums
+ * locally, in group order (bit-exact like the pull path); 0 disables it
+ * (default 256 KiB, env RS_LL_MAX_BYTES, capped by the per-peer area reserved
+ * at creation, env RS_LL_CAPACITY, default 512 KiB). */
 int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value);
 
 /* NVLS (NVLink SHARP): with RS_NVLS=1 at context creation the heaps are

@@ -240,8 +240,10 @@ int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value) {
     ctx->impl->nvls_min_group = static_cast<int>(value);
   } else if (k == "nvls_min_bytes") {
     ctx->impl->nvls_min_bytes = value < 0 ? ~0ull : static_cast<uint64_t>(value);
+  } else if (k == "ll_max_bytes") {
+    ctx->impl->ll_max_bytes = value < 0 ? 0 : static_cast<uint64_t>(value);
   } else {
-    return Bad("unknown option (push_min_bytes | barrier_timeout_ms | nvls | nvls_min_group | nvls_min_bytes)");
+    return Bad("unknown option (push_min_bytes | barrier_timeout_ms | nvls | nvls_min_group | nvls_min_bytes | ll_max_bytes)");
   }
   return RS_OK;
 }

@@ -51,8 +51,8 @@ absl::Status AllocateRank(Context* ctx, int r) {
   RS_CUDA(cudaSetDevice(rank.ordinal));
   int hosted = 0;
   for (int d = 0; d < ctx->K; ++d) hosted += ctx->slot_rank[d] == r;
-  rank.heap_bytes =
-      kDataOffset + static_cast<size_t>(hosted) * (1 + ctx->scratch_regions) * ctx->slot_stride;
+  rank.heap_bytes = kDataOffset + static_cast<size_t>(hosted) * (1 + ctx->scratch_regions) * ctx->slot_stride +
+                    static_cast<size_t>(ctx->world) * 2 * ctx->LLRegionBytes();
   if (ctx->use_vmm) {
     // cuMemCreate'd heap: shareable as a POSIX fd and bindable to multicast.
     std::vector<int> access{rank.ordinal};
@@ -70,6 +70,9 @@ absl::Status AllocateRank(Context* ctx, int r) {
     rank.heap = static_cast<char*>(heap);
   }
   RS_CUDA(cudaMemset(rank.heap, 0, kDataOffset));
+  if (ctx->ll_capacity > 0) {
+    RS_CUDA(cudaMemset(rank.heap + ctx->ll_offset[r], 0, static_cast<size_t>(ctx->world) * 2 * ctx->LLRegionBytes()));
+  }
   const uint64_t first_epoch = 1;
   RS_CUDA(cudaMemcpy(rank.heap + kEpochOffset, &first_epoch, sizeof(first_epoch), cudaMemcpyHostToDevice));
   RS_CUDA(cudaStreamCreateWithFlags(&rank.stream, cudaStreamNonBlocking));
@@ -98,6 +101,18 @@ void AssignPositions(Context* ctx) {
   if (const char* env = std::getenv("RS_SCRATCH_REGIONS")) {
     const int v = std::atoi(env);
     if (v >= 0) ctx->scratch_regions = v;
+  }
+  // One-shot (LL) area after the slots: RS_LL_CAPACITY payload bytes per
+  // (sender, parity) region (0 disables); RS_LL_MAX_BYTES the step budget.
+  if (ctx->world > 1) {
+    ctx->ll_capacity = 512u << 10;
+    ctx->ll_max_bytes = 256u << 10;
+    if (const char* env = std::getenv("RS_LL_CAPACITY")) ctx->ll_capacity = std::strtoull(env, nullptr, 10) & ~7ull;
+    if (const char* env = std::getenv("RS_LL_MAX_BYTES")) ctx->ll_max_bytes = std::strtoull(env, nullptr, 10);
+  }
+  ctx->ll_offset.assign(ctx->world, 0);
+  for (int r = 0; r < ctx->world; ++r) {
+    ctx->ll_offset[r] = kDataOffset + static_cast<size_t>(next[r]) * (1 + ctx->scratch_regions) * ctx->slot_stride;
   }
 }
 

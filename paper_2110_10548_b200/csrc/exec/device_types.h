@@ -29,6 +29,13 @@ struct Task {
 
 constexpr uint16_t kModeSum = 0;
 constexpr uint16_t kModeNvlsAllReduce = 1;
+// One-shot (LL) task over [lo, hi): pointers tagged with bit 0 are LL packet
+// streams (biased: the packet of byte x at +2x, plus the epoch's parity
+// region). Untagged sources are local slot buffers (at most one: `local`).
+// Tagged destinations receive `local` as packets (sends); untagged
+// destinations receive the sum of the sources in order (tagged sources are
+// waited for by flag). Whole 8-byte packets cover [lo & ~7, round8(hi)).
+constexpr uint16_t kModeLL = 2;
 
 // Everything one rank's kernel for one step needs (passed by value).
 struct StepArgs {
@@ -46,6 +53,8 @@ struct StepArgs {
   uint32_t nwait;
   uint32_t nfinal;
   uint32_t has_nvls;  // any multimem task: order unicast/multicast aliases (fence.proxy.alias)
+  uint32_t has_ll;    // any one-shot task: launch the LL instantiation
+  uint32_t signal_done;  // some peer waits for this step's epoch (else no exit fence)
   uint8_t wait_ranks[RS_MAX_RANKS];
   uint8_t final_ranks[RS_MAX_RANKS];
   // Epochs are relative to a device-resident run base (so a captured CUDA
@@ -56,11 +65,15 @@ struct StepArgs {
   uint32_t step;
   uint32_t num_steps;
   uint64_t timeout_ns;
+  uint64_t ll_parity_stride;  // bytes between the two parity regions of an LL block
 };
 
 // Vector work is cut into pieces of kPieceBytes; a CTA walks a piece in
 // chunks of threads * unroll * 16 bytes.
 constexpr uint32_t kPieceBytes = 64u << 10;
+// LL pieces: 8 packets (64 payload bytes) per thread of a 512-thread CTA,
+// all in flight at once.
+constexpr uint32_t kLLPieceBytes = 32u << 10;
 
 cudaError_t LaunchStep(const StepArgs& args, int grid, int block, int unroll, cudaStream_t stream);
 

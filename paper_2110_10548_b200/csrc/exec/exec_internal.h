@@ -25,6 +25,9 @@ namespace rs {
 //   [2 MiB, ...)   per hosted slot: its buffer, then `scratch_regions`
 //                  scratch buffers (landing zones of the push variant), each
 //                  slot_stride bytes (max_bytes rounded up to 2 MiB)
+//   then           the one-shot (LL) receive area when world > 1: per sender
+//                  rank, two parity regions of 2 * ll_capacity bytes (16-byte
+//                  packets {data0, flag, data1, flag} carry 8 payload bytes)
 constexpr size_t kInboxOffset = 0;
 constexpr size_t kCounterOffset = 256;
 constexpr size_t kErrorOffset = 512;
@@ -58,11 +61,19 @@ typedef int (*ExchangeFn)(const void* send, size_t bytes, void* recv, void* user
 // A pointer-table entry: slot `slot`'s buffer (region -1) or its scratch
 // region `region`.
 constexpr int kMcRegion = -2;  // Ref{mc group index, kMcRegion}: a multicast base
+// Ref{source slot, kLLRegion, receiver, sender, off}: packets of the source
+// slot's data in the receiver rank's LL area, sender's block, parity-0
+// region, biased so that the packet of payload byte x sits at +2x (the kernel
+// adds the parity). Tagged with bit 0 in the pointer table.
+constexpr int kLLRegion = -3;
 constexpr size_t kMaxMcGroups = 32;  // multicast objects per context (switch resources)
 
 struct Ref {
   int slot;    // slot id, or mc group index for kMcRegion
-  int region;  // -1 buffer, >= 0 scratch region, kMcRegion multicast
+  int region;  // -1 buffer, >= 0 scratch region, kMcRegion multicast, kLLRegion
+  int ll_recv = 0;
+  int ll_send = 0;
+  int64_t ll_off = 0;
   friend bool operator==(const Ref&, const Ref&) = default;
   friend auto operator<=>(const Ref&, const Ref&) = default;
 };
@@ -96,6 +107,15 @@ class Context {
   // Below this many bytes per group the P2P kernel's lower latency wins
   // (measured crossover ~16 MiB at n = 4, profiles/r01_sweep_n4_bf16_graph_nvls.json).
   uint64_t nvls_min_bytes = 16ull << 20;
+  // One-shot (LL) steps: when every cross-GPU group of a step has its members
+  // on distinct GPUs and each GPU sends any peer at most ll_max_bytes, the
+  // step runs as one kernel in which every owner receives its sources as
+  // flagged packets pushed into its own LL area and sums locally: no remote
+  // loads, no tail wait (latency-bound sizes). ll_capacity is fixed at
+  // creation (RS_LL_CAPACITY); ll_max_bytes is a run-time option.
+  uint64_t ll_capacity = 0;
+  uint64_t ll_max_bytes = 0;
+  std::vector<size_t> ll_offset;  // per rank: its LL area within its heap
   ExchangeFn exchange = nullptr;  // host all-gather (multi-process NVLS setup)
   void* exchange_user = nullptr;
   std::map<std::vector<int>, std::unique_ptr<McGroup>> mc_groups;
@@ -105,8 +125,14 @@ class Context {
            (static_cast<size_t>(slot_position[slot]) * (1 + scratch_regions) + 1 + region) * slot_stride;
   }
   std::vector<McGroup*> mc_index;  // Ref{i, kMcRegion} -> group
+  uint64_t LLRegionBytes() const { return 2 * ll_capacity; }
   char* RefPtr(int viewer, const Ref& r) const {
     if (r.region == kMcRegion) return reinterpret_cast<char*>(mc_index[r.slot]->va[viewer]);
+    if (r.region == kLLRegion) {
+      const uintptr_t p = reinterpret_cast<uintptr_t>(ranks[viewer].view[r.ll_recv]) + ll_offset[r.ll_recv] +
+                          static_cast<uintptr_t>(r.ll_send) * 2 * LLRegionBytes() + static_cast<uintptr_t>(r.ll_off);
+      return reinterpret_cast<char*>(p | 1u);
+    }
     return ranks[viewer].view[slot_rank[r.slot]] + SlotOffset(r.slot, r.region);
   }
   char* SlotPtr(int viewer, int slot) const { return RefPtr(viewer, Ref{slot, -1}); }
@@ -119,7 +145,9 @@ struct RankStep {
   std::vector<Ref> ptr_refs;  // pointer-table entries
   uint32_t npieces = 0;
   uint32_t piece_bytes = kPieceBytes;  // 4 KiB .. 64 KiB, sized to fill the GPU
+  uint32_t max_grid = 0;      // 0 = resident capacity (one-shot phases: a few CTAs)
   std::vector<uint8_t> wait;  // ranks to wait for before the phase
+  bool signal_done = true;    // a peer waits for this rank's end-of-phase epoch
   double tx_bytes = 0, rx_bytes = 0, hbm_bytes = 0;
 };
 
@@ -138,6 +166,7 @@ class Plan {
   // variant: scatter into owners' scratch, then reduce + push results).
   std::vector<std::vector<RankStep>> phases;  // [phase][rank]
   std::vector<int> phase_step;                // program step of each phase
+  std::vector<uint8_t> phase_ll;              // 1: one-shot (LL) phase
   std::vector<uint8_t> final_wait_bits;       // per rank: ranks for the tail wait
   // Device copies (per driven rank): all tasks / pointer tables of all phases.
   std::vector<Task*> d_tasks;

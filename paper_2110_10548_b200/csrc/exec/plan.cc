@@ -23,6 +23,7 @@
 #include <memory>
 #include <cstdlib>
 #include <set>
+#include <tuple>
 
 #include "absl/strings/str_format.h"
 #include "exec_internal.h"
@@ -121,6 +122,13 @@ std::vector<std::vector<Range>> SplitEven(const std::vector<Range>& ranges, int 
 std::vector<int> HeldRows(const redsynth::StateContext& st, int d) {
   return st.state(d).NonEmptyRows();
 }
+
+// One-shot destination: owner[range] = sum of src[range] in order.
+struct LLSpec {
+  int owner;
+  Range range;
+  std::vector<int> src;
+};
 
 // Task lists of the two phases of one program step.
 struct StepTasks {
@@ -236,6 +244,70 @@ struct Compiler {
     for (int d : g) ranks.push_back(ctx->slot_rank[d]);
     std::sort(ranks.begin(), ranks.end());
     return std::adjacent_find(ranks.begin(), ranks.end()) == ranks.end();
+  }
+
+  // One-shot form of a group (LL steps): every destination slot computes its
+  // own result from all sources (no owner slicing, no fan-out), so each
+  // source's bytes cross NVLink exactly once per receiving GPU. Content ids
+  // evolve exactly as in Group().
+  void GroupLL(std::vector<LLSpec>& out, const redsynth::StateContext& pre, const std::vector<int>& g,
+               redsynth::Collective op) {
+    using redsynth::Collective;
+    const int n = static_cast<int>(g.size());
+    auto add = [&](int owner, const std::vector<Range>& ranges, const std::vector<int>& src) {
+      for (const Range& r : ranges) out.push_back(LLSpec{owner, r, src});
+    };
+    switch (op) {
+      case Collective::kAllReduce: {
+        const std::vector<int> rows = HeldRows(pre, g[0]);
+        const std::vector<Range> ranges = geo.Ranges(rows);
+        for (int m : g) add(m, ranges, g);
+        for (int r : rows) {
+          const uint64_t id = next_id++;
+          for (int m : g) Vid(m, r) = id;
+        }
+        break;
+      }
+      case Collective::kReduceScatter: {
+        const std::vector<int> rows = HeldRows(pre, g[0]);
+        const int run = n ? static_cast<int>(rows.size()) / n : 0;
+        if (run == 0) break;
+        for (int m = 0; m < n; ++m)
+          add(g[m], geo.Ranges(std::vector<int>(rows.begin() + m * run, rows.begin() + (m + 1) * run)), g);
+        for (int m = 0; m < n; ++m)
+          for (int i = m * run; i < (m + 1) * run; ++i) Vid(g[m], rows[i]) = next_id++;
+        break;
+      }
+      case Collective::kReduce: {
+        const std::vector<int> rows = HeldRows(pre, g[0]);
+        add(g[0], geo.Ranges(rows), g);
+        for (int r : rows) Vid(g[0], r) = next_id++;
+        break;
+      }
+      case Collective::kAllGather:
+      case Collective::kBroadcast: {
+        std::vector<std::pair<int, int>> row_holder;
+        if (op == Collective::kAllGather) {
+          for (int r = 0; r < K; ++r)
+            for (int m : g)
+              if (!pre.state(m).RowEmpty(r)) row_holder.push_back({r, m});
+        } else {
+          for (int r : HeldRows(pre, g[0])) row_holder.push_back({r, g[0]});
+        }
+        // (holder, receiver) -> rows, decided on the pre-step content ids.
+        std::map<std::pair<int, int>, std::vector<int>> rows_of;
+        for (auto [r, h] : row_holder)
+          for (int m : g)
+            if (m != h && Vid(m, r) != Vid(h, r)) rows_of[{h, m}].push_back(r);
+        for (auto& [hm, rows] : rows_of) {
+          std::sort(rows.begin(), rows.end());
+          add(hm.second, geo.Ranges(rows), {hm.first});
+        }
+        for (auto& [hm, rows] : rows_of)
+          for (int r : rows) Vid(hm.second, r) = Vid(hm.first, r);
+        break;
+      }
+    }
   }
 
   absl::Status Group(StepTasks& out, const redsynth::StateContext& pre, const std::vector<int>& g,
@@ -392,6 +464,130 @@ void Lay(RankStep& rs, const ProtoTask& t, uint32_t piece_bytes) {
   push(b, t.range.hi, false);
 }
 
+// Lays a one-shot step into `phase` (one RankStep per rank). Returns false
+// (phase untouched) when the step does not fit the LL scheme: a cross-GPU
+// group with two members on one GPU, a GPU pair exchanging more than the LL
+// budget, or a send whose bytes another task of the step overwrites.
+bool LayLL(const Context& ctx, const std::vector<LLSpec>& specs, std::vector<RankStep>& phase) {
+  const int R = ctx.world;
+  const uint64_t budget = std::min<uint64_t>(ctx.ll_max_bytes, ctx.ll_capacity);
+  auto lo8 = [](const Range& r) { return r.lo & ~uint64_t{7}; };
+  auto hi8 = [](const Range& r) { return (r.hi + 7) & ~uint64_t{7}; };
+  // Payload streams: (sender rank, receiver rank, source slot, lo, hi) -> offset.
+  std::map<std::tuple<int, int, int, uint64_t, uint64_t>, uint64_t> stream;
+  std::vector<uint64_t> pair_bytes(static_cast<size_t>(R) * R, 0);
+  for (const LLSpec& sp : specs) {
+    const int p = ctx.slot_rank[sp.owner];
+    int locals = 0;
+    for (int x : sp.src) {
+      const int q = ctx.slot_rank[x];
+      if (q == p) {
+        ++locals;
+        continue;
+      }
+      auto key = std::make_tuple(q, p, x, sp.range.lo, sp.range.hi);
+      if (stream.count(key)) continue;
+      uint64_t& used = pair_bytes[static_cast<size_t>(q) * R + p];
+      stream[key] = used;
+      used += hi8(sp.range) - lo8(sp.range);
+      if (used > budget) return false;
+    }
+    if (locals > 1) return false;
+  }
+  auto ll_ref = [&](int slot, int recv, int send, uint64_t off, const Range& rg) {
+    Ref r{slot, kLLRegion};
+    r.ll_recv = recv;
+    r.ll_send = send;
+    r.ll_off = 2 * static_cast<int64_t>(off) - 2 * static_cast<int64_t>(lo8(rg));
+    return r;
+  };
+  // Receive tasks, one per spec; a source that is itself the owner of the
+  // same range (AllReduce) sends its packets from inside its own task, so the
+  // value it sends is read before the task overwrites it.
+  struct Proto {
+    int rank;
+    Range range;
+    std::vector<Ref> src, dst;
+  };
+  std::vector<Proto> recv;
+  std::map<std::tuple<int, uint64_t, uint64_t>, size_t> fused;  // (owner, lo, hi) -> recv index
+  for (const LLSpec& sp : specs) {
+    const int p = ctx.slot_rank[sp.owner];
+    Proto t{p, sp.range, {}, {Buf(sp.owner)}};
+    for (int x : sp.src) {
+      const int q = ctx.slot_rank[x];
+      t.src.push_back(q == p ? Buf(x) : ll_ref(x, p, q, stream[{q, p, x, sp.range.lo, sp.range.hi}], sp.range));
+    }
+    if (std::find(sp.src.begin(), sp.src.end(), sp.owner) != sp.src.end())
+      fused[{sp.owner, sp.range.lo, sp.range.hi}] = recv.size();
+    recv.push_back(std::move(t));
+  }
+  std::vector<Proto> sends;
+  std::map<std::tuple<int, uint64_t, uint64_t>, size_t> send_index;  // (slot, lo, hi) -> sends index
+  for (const auto& [key, off] : stream) {
+    const auto [q, p, x, lo, hi] = key;
+    const Range rg{lo, hi};
+    const Ref dst = ll_ref(x, p, q, off, rg);
+    auto f = fused.find({x, lo, hi});
+    if (f != fused.end()) {
+      recv[f->second].dst.push_back(dst);
+      continue;
+    }
+    auto it = send_index.find({x, lo, hi});
+    if (it == send_index.end()) {
+      it = send_index.emplace(std::make_tuple(x, lo, hi), sends.size()).first;
+      sends.push_back(Proto{q, rg, {Buf(x)}, {}});
+    }
+    sends[it->second].dst.push_back(dst);
+  }
+  // A separate send reads its slot during the step: nothing may write its
+  // range (the padding bytes of edge packets are ignored by the receivers).
+  for (const Proto& sd : sends) {
+    const int x = sd.src[0].slot;
+    for (const LLSpec& sp : specs) {
+      if (sp.owner == x && sp.range.lo < sd.range.hi && sd.range.lo < sp.range.hi) return false;
+    }
+  }
+  auto lay = [&](const Proto& t) {
+    RankStep& rs = phase[t.rank];
+    Task task{};
+    task.lo = t.range.lo;
+    task.hi = t.range.hi;
+    task.piece_begin = rs.npieces;
+    task.ptr_begin = static_cast<uint32_t>(rs.ptr_refs.size());
+    task.nsrc = static_cast<uint16_t>(t.src.size());
+    task.ndst = static_cast<uint16_t>(t.dst.size());
+    task.vec = 1;
+    task.mode = kModeLL;
+    rs.ptr_refs.insert(rs.ptr_refs.end(), t.src.begin(), t.src.end());
+    rs.ptr_refs.insert(rs.ptr_refs.end(), t.dst.begin(), t.dst.end());
+    const uint64_t span = hi8(t.range) - lo8(t.range);
+    rs.npieces += static_cast<uint32_t>((span + kLLPieceBytes - 1) / kLLPieceBytes);
+    rs.tasks.push_back(task);
+    rs.hbm_bytes += static_cast<double>(t.range.hi - t.range.lo);
+    for (const Ref& d : t.dst) {
+      if (d.region != kLLRegion) {
+        rs.hbm_bytes += static_cast<double>(t.range.hi - t.range.lo);
+        continue;
+      }
+      rs.tx_bytes += 2.0 * static_cast<double>(span);
+      phase[d.ll_recv].rx_bytes += 2.0 * static_cast<double>(span);
+    }
+  };
+  for (const Proto& t : sends) lay(t);  // sends first: peers wait on them
+  for (const Proto& t : recv) lay(t);
+  // Few CTAs: each pays one round trip for all its packets, and a one-CTA
+  // launch skips the cross-CTA exit barrier (profiles/r01_ll_sweep_n2.txt).
+  uint64_t cta_bytes = 32u << 10;
+  if (const char* env = std::getenv("RS_LL_CTA_BYTES")) cta_bytes = std::max<uint64_t>(8, std::strtoull(env, nullptr, 10));
+  std::vector<uint64_t> span_bytes(R, 0);
+  for (const std::vector<Proto>* list : {&sends, &recv})
+    for (const Proto& t : *list) span_bytes[t.rank] += hi8(t.range) - lo8(t.range);
+  for (int r = 0; r < R; ++r)
+    phase[r].max_grid = static_cast<uint32_t>(std::max<uint64_t>(1, (span_bytes[r] + cta_bytes - 1) / cta_bytes));
+  return true;
+}
+
 absl::Status Upload(const void* host, size_t bytes, void** dev, const char* what) {
   absl::Status s = CudaStatus(cudaMalloc(dev, bytes), what);
   if (!s.ok()) return s;
@@ -506,8 +702,44 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
   for (int s = 0; s < num_steps; ++s) {
     StepTasks tasks;
     const redsynth::CollectiveStep& step = lowered.steps[s];
-    for (size_t gi = 0; gi < step.groups.size(); ++gi) {
+    for (size_t gi = 0; gi < step.groups.size(); ++gi)
       for (int d : step.groups[gi]) gidx[s][d] = static_cast<int>(gi);
+    // One-shot (LL) attempt: cross-GPU groups as LLSpecs, GPU-local groups as
+    // ordinary tasks, all in one launch; on any misfit roll back the content
+    // ids and take the pull / push / NVLS path.
+    if (R > 1 && ctx->ll_capacity > 0 && ctx->ll_max_bytes > 0) {
+      const std::vector<uint64_t> saved_vid = comp.vid;
+      const uint64_t saved_next = comp.next_id;
+      std::vector<LLSpec> specs;
+      StepTasks local;
+      for (const std::vector<int>& g : step.groups) {
+        if (comp.SpansRanks(g)) {
+          comp.GroupLL(specs, pre[s], g, step.op);
+        } else {
+          absl::Status gs = comp.Group(local, pre[s], g, step.op);
+          if (!gs.ok()) return gs;
+        }
+      }
+      std::vector<RankStep> phase(R);
+      bool ok = local.a.empty() && !specs.empty();
+      if (ok) {
+        for (int r = 0; r < R; ++r) phase[r].piece_bytes = kLLPieceBytes;
+        ok = LayLL(*ctx, specs, phase);
+      }
+      if (ok) {
+        for (const ProtoTask& t : local.b) {
+          AddTraffic(phase, *ctx, t);
+          Lay(phase[ctx->slot_rank[t.owner]], t, kLLPieceBytes);
+        }
+        plan->phases.push_back(std::move(phase));
+        plan->phase_step.push_back(s);
+        plan->phase_ll.push_back(1);
+        continue;
+      }
+      comp.vid = saved_vid;
+      comp.next_id = saved_next;
+    }
+    for (size_t gi = 0; gi < step.groups.size(); ++gi) {
       absl::Status gs = comp.Group(tasks, pre[s], step.groups[gi], step.op);
       if (!gs.ok()) return gs;
     }
@@ -515,6 +747,7 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
       if (list == &tasks.a && list->empty()) continue;
       plan->phases.emplace_back(R);
       plan->phase_step.push_back(s);
+      plan->phase_ll.push_back(0);
       // Piece size per rank: enough pieces to occupy ~2 CTAs per SM (memory
       // parallelism for remote loads), between 4 KiB and kPieceBytes.
       std::vector<uint64_t> rank_bytes(R, 0);
@@ -553,13 +786,33 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
       plan->phases[ph][r].wait.assign(wait.begin(), wait.end());
     }
   }
-  if (P > 0) {
+  // A one-shot last phase writes only its own GPU's slots: no tail wait.
+  if (P > 0 && !plan->phase_ll[P - 1]) {
     for (int d = 0; d < K; ++d) {
       const int r = ctx->slot_rank[d];
       for (int p : group_of(P - 1, d)) {
         const int q = ctx->slot_rank[p];
         if (q != r) plan->final_wait_bits[r] |= static_cast<uint8_t>(1u << q);
       }
+    }
+  }
+
+  // End-of-phase epochs nobody waits for are not published (the exit fence
+  // is most of a small step's cost): phase ph's epoch is awaited by the next
+  // phase's entry sets, or, for the last phase, by the tail waits.
+  for (int ph = 0; ph < P; ++ph) {
+    for (int r = 0; r < R; ++r) {
+      bool needed = false;
+      for (int q = 0; q < R && !needed; ++q) {
+        if (q == r) continue;
+        if (ph + 1 < P) {
+          const std::vector<uint8_t>& w = plan->phases[ph + 1][q].wait;
+          needed = std::find(w.begin(), w.end(), static_cast<uint8_t>(r)) != w.end();
+        } else {
+          needed = (plan->final_wait_bits[q] >> r) & 1u;
+        }
+      }
+      plan->phases[ph][r].signal_done = needed;
     }
   }
 
@@ -651,6 +904,7 @@ absl::Status RunPlan(Plan* plan, void* const* device_bufs, void* const* host_buf
       a.error_flag = reinterpret_cast<int*>(rank.heap + kErrorOffset);
       a.inbox = reinterpret_cast<const uint64_t*>(rank.heap + kInboxOffset);
       a.timeout_ns = ctx->timeout_ns;
+      a.ll_parity_stride = ctx->LLRegionBytes();
       if (ctx->world > 1) {
         for (int q = 0; q < ctx->world; ++q) {
           if (q == r) continue;
@@ -662,12 +916,17 @@ absl::Status RunPlan(Plan* plan, void* const* device_bufs, void* const* host_buf
             if (plan->final_wait_bits[r] & (1u << q)) a.final_ranks[a.nfinal++] = static_cast<uint8_t>(q);
         }
       }
+      a.signal_done = rsx.signal_done ? 1u : 0u;
       a.epoch_base = reinterpret_cast<uint64_t*>(rank.heap + kEpochOffset);
       a.step = static_cast<uint32_t>(ph);
       a.num_steps = static_cast<uint32_t>(P);
-      for (const Task& t : rsx.tasks) a.has_nvls |= t.mode == kModeNvlsAllReduce ? 1u : 0u;
+      for (const Task& t : rsx.tasks) {
+        a.has_nvls |= t.mode == kModeNvlsAllReduce ? 1u : 0u;
+        a.has_ll |= t.mode == kModeLL ? 1u : 0u;
+      }
       const int resident = plan->ctas_per_sm * rank.sm_count;
       int cap = plan->max_ctas > 0 ? std::min(plan->max_ctas, resident) : resident;
+      if (rsx.max_grid > 0) cap = std::min<int>(cap, static_cast<int>(rsx.max_grid));
       if (cap <= 0) cap = 148;
       const int grid = std::max(1, std::min<int>(cap, static_cast<int>(rsx.npieces)));
       absl::Status st = CudaStatus(cudaSetDevice(rank.ordinal), "cudaSetDevice");
@@ -685,6 +944,7 @@ std::string DescribePlan(const Plan& plan) {
   doc["num_steps"] = plan.num_steps;
   doc["num_phases"] = plan.num_phases();
   doc["phase_step"] = plan.phase_step;
+  doc["phase_ll"] = plan.phase_ll;
   doc["bytes"] = plan.bytes;
   doc["world"] = plan.ctx->world;
   doc["slot_rank"] = plan.ctx->slot_rank;
@@ -695,11 +955,21 @@ std::string DescribePlan(const Plan& plan) {
     for (const RankStep& r : per_rank) {
       nlohmann::ordered_json tasks = nlohmann::ordered_json::array();
       for (const Task& t : r.tasks) {
-        std::vector<int> src, dst, src_region, dst_region;
+        std::vector<int> src, dst, src_region, dst_region, sends;
         for (int i = 0; i < t.nsrc + t.ndst; ++i) {
           const Ref& ref = r.ptr_refs[t.ptr_begin + i];
+          if (i >= t.nsrc && ref.region == kLLRegion) {
+            sends.push_back(ref.ll_recv);  // packets of the local source to that rank
+            continue;
+          }
           (i < t.nsrc ? src : dst).push_back(ref.slot);
           (i < t.nsrc ? src_region : dst_region).push_back(ref.region);
+        }
+        if (t.mode == kModeLL) {
+          tasks.push_back({{"lo", t.lo}, {"hi", t.hi}, {"vec", t.vec}, {"mode", t.mode},
+                           {"piece_begin", t.piece_begin}, {"src", src}, {"dst", dst}, {"src_region", src_region},
+                           {"dst_region", dst_region}, {"sends", sends}});
+          continue;
         }
         if (t.mode == kModeNvlsAllReduce) {
           const McGroup* mc = plan.ctx->mc_index[r.ptr_refs[t.ptr_begin].slot];
@@ -715,7 +985,7 @@ std::string DescribePlan(const Plan& plan) {
                          {"dst_region", dst_region}});
       }
       std::vector<int> wait(r.wait.begin(), r.wait.end());
-      ranks.push_back({{"wait", wait}, {"npieces", r.npieces}, {"tx", r.tx_bytes}, {"rx", r.rx_bytes},
+      ranks.push_back({{"wait", wait}, {"signal", r.signal_done}, {"npieces", r.npieces}, {"tx", r.tx_bytes}, {"rx", r.rx_bytes},
                        {"hbm", r.hbm_bytes}, {"tasks", tasks}});
     }
     phases.push_back({{"ranks", ranks}});

@@ -54,7 +54,22 @@ __device__ __forceinline__ void StoreReleaseSys(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ void StoreRelaxedSys(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ void FenceSys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
+// Flag stores: RS_SYNC_STRICT=1 restores release stores behind extra fences
+// (A/B of the barrier cost); the default orders data before flags with one
+// system fence per CTA plus one in the last CTA, then relaxed flag stores.
+#ifndef RS_SYNC_STRICT
+#define RS_SYNC_STRICT 0
+#endif
+__device__ __forceinline__ void SignalStore(uint64_t* p, uint64_t v) {
+  if (RS_SYNC_STRICT) StoreReleaseSys(p, v);
+  else StoreRelaxedSys(p, v);
+}
 
 __device__ __forceinline__ uint64_t GlobalTimer() {
   uint64_t t;
@@ -255,14 +270,196 @@ __device__ void ScalarTask(const Task& t, void* const* ptrs) {
   }
 }
 
-template <int DT, int kUnroll>
+// ---- one-shot (LL) tasks -------------------------------------------------
+
+__device__ __forceinline__ void StoreLL(char* p, uint2 d, uint32_t flag) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(d.x), "r"(flag), "r"(d.y),
+               "r"(flag)
+               : "memory");
+}
+
+// Waits for the packet at p to carry `flag` in both halves (each 8-byte half
+// {data, flag} lands atomically), returns its payload.
+__device__ __forceinline__ uint2 LoadLL(const char* p, uint32_t flag, uint64_t timeout_ns, int* error_flag) {
+  uint32_t d0, f0, d1, f1;
+  uint64_t t0 = 0;
+  for (uint32_t spin = 0;; ++spin) {
+    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(d0), "=r"(f0), "=r"(d1), "=r"(f1)
+                 : "l"(p)
+                 : "memory");
+    if (f0 == flag && f1 == flag) break;
+    if (spin == 4096) t0 = GlobalTimer();
+    if (spin > 4096 && (spin & 63) == 0 && GlobalTimer() - t0 > timeout_ns) {
+      atomicExch(error_flag, 1);
+      break;
+    }
+  }
+  return make_uint2(d0, d1);
+}
+
+template <int DT>
+__device__ __forceinline__ uint2 AddPacket(uint2 a, uint2 b) {
+  if constexpr (DT == RS_BF16) {
+    return a;  // bf16 sums are kept in f32 by the caller
+  } else if constexpr (DT == RS_F32) {
+    return make_uint2(__float_as_uint(__fadd_rn(__uint_as_float(a.x), __uint_as_float(b.x))),
+                      __float_as_uint(__fadd_rn(__uint_as_float(a.y), __uint_as_float(b.y))));
+  } else {
+    return make_uint2(a.x + b.x, a.y + b.y);
+  }
+}
+
+// LL task pointers: the (at most one) untagged source is local.
+__device__ __forceinline__ const char* LLLocal(const Task& t, void* const* src) {
+  const char* local = nullptr;
+  for (int i = 0; i < t.nsrc; ++i)
+    if (!(reinterpret_cast<uintptr_t>(src[i]) & 1u)) local = static_cast<const char*>(src[i]);
+  return local;
+}
+
+// Packets per thread in flight in the one-shot sweeps (memory-level
+// parallelism: a thread's packets are independent round trips).
+constexpr int kLLBatch = 8;
+
+__device__ __forceinline__ uint4 LoadVolatile16(const char* p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+
+// Sweep 1 over packets [begin, end) (8-byte aligned payload offsets) of an
+// LL task: push the local source's packets to every tagged destination.
+__device__ __forceinline__ void LLSend(const Task& t, void* const* ptrs, uint64_t begin, uint64_t end,
+                                       uint32_t flag, uint64_t parity_off) {
+  void* const* src = ptrs + t.ptr_begin;
+  void* const* dst = src + t.nsrc;
+  const char* local = LLLocal(t, src);
+  if (!local) return;
+  const uint64_t stride = static_cast<uint64_t>(blockDim.x) * 8u;
+  for (uint64_t x0 = begin + static_cast<uint64_t>(threadIdx.x) * 8u; x0 < end; x0 += stride * kLLBatch) {
+    uint2 mine[kLLBatch];
+#pragma unroll
+    for (int b = 0; b < kLLBatch; ++b) {
+      const uint64_t x = x0 + b * stride;
+      if (x < end) mine[b] = *reinterpret_cast<const uint2*>(local + x);
+    }
+    for (int j = 0; j < t.ndst; ++j) {
+      const uintptr_t d = reinterpret_cast<uintptr_t>(dst[j]);
+      if (!(d & 1u)) continue;
+      char* base = reinterpret_cast<char*>((d & ~uintptr_t{1}) + parity_off);
+#pragma unroll
+      for (int b = 0; b < kLLBatch; ++b) {
+        const uint64_t x = x0 + b * stride;
+        if (x < end) StoreLL(base + 2 * x, mine[b], flag);
+      }
+    }
+  }
+}
+
+// Sweep 2 over the same packets (same thread per packet, so a task that sends
+// its own slot reads every value before overwriting it): wait for the tagged
+// sources, sum all sources in order, store the elements inside [lo, hi).
+template <int DT>
+__device__ __forceinline__ void LLReceive(const Task& t, void* const* ptrs, uint64_t begin, uint64_t end,
+                                          uint32_t flag, uint64_t parity_off, uint64_t timeout_ns,
+                                          int* error_flag) {
+  constexpr uint32_t kEs = DT == RS_BF16 ? 2 : 4;
+  constexpr int kLLBatch = 8;
+  void* const* src = ptrs + t.ptr_begin;
+  void* const* dst = src + t.nsrc;
+  bool any_result = false;
+  for (int j = 0; j < t.ndst; ++j) any_result |= !(reinterpret_cast<uintptr_t>(dst[j]) & 1u);
+  if (!any_result) return;
+  const char* local = LLLocal(t, src);
+  const uint64_t stride = static_cast<uint64_t>(blockDim.x) * 8u;
+  for (uint64_t x0 = begin + static_cast<uint64_t>(threadIdx.x) * 8u; x0 < end; x0 += stride * kLLBatch) {
+    uint2 mine[kLLBatch], out[kLLBatch];
+    float f[kLLBatch][4];
+#pragma unroll
+    for (int b = 0; b < kLLBatch; ++b) {
+      const uint64_t x = x0 + b * stride;
+      mine[b] = (local && x < end) ? *reinterpret_cast<const uint2*>(local + x) : make_uint2(0, 0);
+    }
+    // Sum in source order; a single source is a raw copy.
+    for (int i = 0; i < t.nsrc; ++i) {
+      const uintptr_t s = reinterpret_cast<uintptr_t>(src[i]);
+      uint2 v[kLLBatch];
+      if (s & 1u) {
+        const char* base = reinterpret_cast<const char*>((s & ~uintptr_t{1}) + parity_off);
+        uint4 pk[kLLBatch];
+#pragma unroll
+        for (int b = 0; b < kLLBatch; ++b) {  // all loads in flight at once
+          const uint64_t x = x0 + b * stride;
+          pk[b] = x < end ? LoadVolatile16(base + 2 * x) : make_uint4(0, flag, 0, flag);
+        }
+#pragma unroll
+        for (int b = 0; b < kLLBatch; ++b) {
+          if (pk[b].y != flag || pk[b].w != flag) {
+            const uint2 late = LoadLL(base + 2 * (x0 + b * stride), flag, timeout_ns, error_flag);
+            pk[b] = make_uint4(late.x, flag, late.y, flag);
+          }
+          v[b] = make_uint2(pk[b].x, pk[b].z);
+        }
+      } else {
+#pragma unroll
+        for (int b = 0; b < kLLBatch; ++b) v[b] = mine[b];
+      }
+#pragma unroll
+      for (int b = 0; b < kLLBatch; ++b) {
+        if constexpr (DT == RS_BF16) {
+          float g[4];
+          BF16Acc::Widen(v[b].x, g[0], g[1]);
+          BF16Acc::Widen(v[b].y, g[2], g[3]);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) f[b][k] = i == 0 ? g[k] : __fadd_rn(f[b][k], g[k]);
+        }
+        out[b] = i == 0 ? v[b] : AddPacket<DT>(out[b], v[b]);
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < kLLBatch; ++b) {
+      if constexpr (DT == RS_BF16) {
+        if (t.nsrc > 1) out[b] = make_uint2(BF16Acc::Narrow(f[b][0], f[b][1]), BF16Acc::Narrow(f[b][2], f[b][3]));
+      }
+      const uint64_t x = x0 + b * stride;
+      if (x >= end) continue;
+      const bool whole = x >= t.lo && x + 8 <= t.hi;
+      for (int j = 0; j < t.ndst; ++j) {
+        const uintptr_t d = reinterpret_cast<uintptr_t>(dst[j]);
+        if (d & 1u) continue;
+        char* base = reinterpret_cast<char*>(d);
+        if (whole) {
+          *reinterpret_cast<uint2*>(base + x) = out[b];
+          continue;
+        }
+        // Edge packet: only the elements inside [lo, hi).
+        const char* bytes = reinterpret_cast<const char*>(&out[b]);
+        for (uint32_t e = 0; e < 8; e += kEs) {
+          if (x + e < t.lo || x + e >= t.hi) continue;
+          if (kEs == 2) *reinterpret_cast<uint16_t*>(base + x + e) = *reinterpret_cast<const uint16_t*>(bytes + e);
+          else *reinterpret_cast<uint32_t*>(base + x + e) = *reinterpret_cast<const uint32_t*>(bytes + e);
+        }
+      }
+    }
+  }
+}
+
+// kLL: the phase holds one-shot tasks (a separate instantiation keeps the
+// packet code out of the bulk kernels' register allocation).
+template <int DT, int kUnroll, bool kLL>
 __global__ void __launch_bounds__(512, kUnroll == 4 ? 2 : 1) StepKernel(const __grid_constant__ StepArgs a) {
   // Run base epoch (device resident; advanced by the previous run's last step).
   const uint64_t base = a.nsignal ? *reinterpret_cast<volatile uint64_t*>(a.epoch_base) : 0;
   // 1. First step of a run: publish "my inputs are in place" to every peer.
   if (a.step == 0 && blockIdx.x == 0 && threadIdx.x < a.nsignal) {
-    FenceSys();
-    StoreReleaseSys(a.signal_ptrs[threadIdx.x], base);
+    // Inputs were written by earlier stream work (complete at kernel
+    // boundaries; peers read them through this GPU's L2): no fence needed.
+    if (RS_SYNC_STRICT) FenceSys();
+    SignalStore(a.signal_ptrs[threadIdx.x], base);
   }
   // 2. Entry barrier: the ranks whose buffers this step touches (and whose
   //    previous-step writers) have finished the previous step.
@@ -272,11 +469,36 @@ __global__ void __launch_bounds__(512, kUnroll == 4 ? 2 : 1) StepKernel(const __
   __syncthreads();
   if (a.has_nvls) FenceProxyAlias();
 
-  // 3. Pieces, grid-strided; tasks are ordered by piece_begin.
+  // 3. Pieces, grid-strided; tasks are ordered by piece_begin. One-shot
+  //    phases first push every packet this CTA sends (sweep 1), so each CTA
+  //    pays one NVLink round trip however many pieces it walks.
+  const uint64_t epoch = base + a.step + 1;
+  const uint64_t parity_off = (epoch & 1) * a.ll_parity_stride;
+  auto ll_range = [&](const Task& t, uint32_t p, uint64_t& begin, uint64_t& end) {
+    begin = (t.lo & ~uint64_t{7}) + static_cast<uint64_t>(p - t.piece_begin) * kLLPieceBytes;
+    end = min((t.hi + 7) & ~uint64_t{7}, begin + kLLPieceBytes);
+  };
+  if constexpr (kLL) {
+    uint32_t c = 0;
+    for (uint32_t p = blockIdx.x; p < a.npieces; p += gridDim.x) {
+      while (c + 1 < a.ntasks && a.tasks[c + 1].piece_begin <= p) ++c;
+      const Task& t = a.tasks[c];
+      if (t.mode != kModeLL) continue;
+      uint64_t begin, end;
+      ll_range(t, p, begin, end);
+      LLSend(t, a.ptrs, begin, end, static_cast<uint32_t>(epoch), parity_off);
+    }
+  }
   uint32_t cur = 0;
   for (uint32_t p = blockIdx.x; p < a.npieces; p += gridDim.x) {
     while (cur + 1 < a.ntasks && a.tasks[cur + 1].piece_begin <= p) ++cur;
     const Task& t = a.tasks[cur];
+    if (kLL && t.mode == kModeLL) {
+      uint64_t begin, end;
+      ll_range(t, p, begin, end);
+      LLReceive<DT>(t, a.ptrs, begin, end, static_cast<uint32_t>(epoch), parity_off, a.timeout_ns, a.error_flag);
+      continue;
+    }
     if (t.vec) {
       const uint64_t begin = t.lo + static_cast<uint64_t>(p - t.piece_begin) * a.piece_bytes;
       const uint64_t end = min(t.hi, begin + a.piece_bytes);
@@ -293,22 +515,30 @@ __global__ void __launch_bounds__(512, kUnroll == 4 ? 2 : 1) StepKernel(const __
     }
   }
 
-  // 4. Exit: the last CTA to finish publishes the step's epoch to all ranks.
-  if (a.nsignal == 0 && a.nfinal == 0) return;
+  // 4. Exit: the last CTA to finish publishes the step's epoch to all ranks
+  //    (skipped when no peer waits for it, e.g. after a one-shot last step).
+  const bool last_step = a.step + 1 == a.num_steps;
+  if (a.nsignal == 0) return;  // one GPU: no epochs
+  if (!a.signal_done && !last_step) return;
   // The CTA barrier orders every thread's stores before thread 0's system
   // fence (cumulativity); one fence per CTA instead of one per thread.
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (a.has_nvls) FenceProxyAlias();
-    FenceSys();
+    const bool publish = a.signal_done;
+    if (publish) {
+      if (a.has_nvls) FenceProxyAlias();
+      FenceSys();
+    }
     const bool last = gridDim.x == 1 || atomicAdd(a.arrive_counter, 1u) == gridDim.x - 1;
     if (last) {
       if (gridDim.x > 1) atomicExch(a.arrive_counter, 0u);
-      FenceSys();
-      for (uint32_t q = 0; q < a.nsignal; ++q) StoreReleaseSys(a.signal_ptrs[q], base + a.step + 1);
+      if (publish) {
+        if (RS_SYNC_STRICT || gridDim.x > 1) FenceSys();  // acquire the other CTAs' releases
+        for (uint32_t q = 0; q < a.nsignal; ++q) SignalStore(a.signal_ptrs[q], base + a.step + 1);
+      }
       // 5. Last step: the run is complete here only once every rank that
       //    writes into our slots has finished too; then advance the base.
-      if (a.step + 1 == a.num_steps) {
+      if (last_step) {
         for (uint32_t i = 0; i < a.nfinal; ++i) {
           WaitAtLeast(a.inbox + a.final_ranks[i], base + a.num_steps, a.timeout_ns, a.error_flag);
         }
@@ -323,9 +553,9 @@ int Occupancy(int dtype, int threads) {
   int blocks = 0;
   cudaError_t e = cudaSuccess;
   switch (dtype) {
-    case RS_F32: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_F32, U>, threads, 0); break;
-    case RS_BF16: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_BF16, U>, threads, 0); break;
-    default: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_I32, U>, threads, 0); break;
+    case RS_F32: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_F32, U, false>, threads, 0); break;
+    case RS_BF16: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_BF16, U, false>, threads, 0); break;
+    default: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_I32, U, false>, threads, 0); break;
   }
   if (e != cudaSuccess || blocks < 1) {
     cudaGetLastError();
@@ -334,12 +564,12 @@ int Occupancy(int dtype, int threads) {
   return blocks;
 }
 
-template <int U>
+template <int U, bool LL>
 cudaError_t Launch(const StepArgs& a, int grid, int block, cudaStream_t stream) {
   switch (a.dtype) {
-    case RS_F32: StepKernel<RS_F32, U><<<grid, block, 0, stream>>>(a); break;
-    case RS_BF16: StepKernel<RS_BF16, U><<<grid, block, 0, stream>>>(a); break;
-    case RS_I32: StepKernel<RS_I32, U><<<grid, block, 0, stream>>>(a); break;
+    case RS_F32: StepKernel<RS_F32, U, LL><<<grid, block, 0, stream>>>(a); break;
+    case RS_BF16: StepKernel<RS_BF16, U, LL><<<grid, block, 0, stream>>>(a); break;
+    case RS_I32: StepKernel<RS_I32, U, LL><<<grid, block, 0, stream>>>(a); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -352,7 +582,8 @@ int MaxResidentCtas(int dtype, int threads, int unroll) {
 }
 
 cudaError_t LaunchStep(const StepArgs& args, int grid, int block, int unroll, cudaStream_t stream) {
-  return unroll == 8 ? Launch<8>(args, grid, block, stream) : Launch<4>(args, grid, block, stream);
+  if (args.has_ll) return Launch<2, true>(args, grid, block, stream);  // (512, 1): 128 registers
+  return unroll == 8 ? Launch<8, false>(args, grid, block, stream) : Launch<4, false>(args, grid, block, stream);
 }
 
 }  // namespace rs

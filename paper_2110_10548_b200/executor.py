@@ -239,7 +239,8 @@ class Context:
 
     def set_option(self, key: str, value: int):
         """Context knobs for later compiles: push_min_bytes (-1 = never push),
-        barrier_timeout_ms."""
+        barrier_timeout_ms, nvls, nvls_min_group, nvls_min_bytes, ll_max_bytes
+        (one-shot budget per GPU pair and step; 0 = never)."""
         nat.check(nat.lib().rs_ctx_set_option(self._h, key.encode(), int(value)))
 
     def synchronize(self):

@@ -37,6 +37,9 @@ def bf16_widen(u16):
     return (u16.astype(np.uint32) << 16).view(np.float32)
 
 
+LL_REGION = -3
+
+
 def simulate_plan(desc, bufs, dtype):
     """Executes a compiled plan (Plan.describe()) over numpy slot buffers.
 
@@ -59,13 +62,27 @@ def simulate_plan(desc, bufs, dtype):
 
     for step in desc["steps"]:
         tasks = [t for r in step["ranks"] for t in r["tasks"]]
+        for rank, r in enumerate(step["ranks"]):
+            for t in r["tasks"]:
+                t["rank"] = rank
         for t in tasks:
             t.setdefault("src_region", [-1] * len(t["src"]))
             t.setdefault("dst_region", [-1] * len(t["dst"]))
+        # One-shot (LL) sources (region -3) are packets of the source slot that
+        # some task on the source's GPU read and sent to this task's GPU.
+        for t in tasks:
+            for s, rg in zip(t["src"], t["src_region"]):
+                if rg != LL_REGION:
+                    continue
+                assert any(u["mode"] == 2 and (s, -1) in zip(u["src"], u["src_region"]) and
+                           (u["lo"], u["hi"]) == (t["lo"], t["hi"]) and t["rank"] in u["sends"]
+                           for u in tasks), f"no sender for LL source {s} of {t}"
         # hazard check: per memory object, written intervals vs every other task's accesses
         acc = {}
         for i, t in enumerate(tasks):
             for s, rg in zip(t["src"], t["src_region"]):
+                if rg == LL_REGION:
+                    continue
                 acc.setdefault((s, rg), []).append((t["lo"], t["hi"], i, "r"))
             for d, rg in zip(t["dst"], t["dst_region"]):
                 acc.setdefault((d, rg), []).append((t["lo"], t["hi"], i, "w"))
@@ -77,14 +94,27 @@ def simulate_plan(desc, bufs, dtype):
                         break
                     if ivs[a][2] != ivs[b][2] and "w" in (ivs[a][3], ivs[b][3]):
                         raise AssertionError(f"hazard on slot {slot}: {ivs[a]} vs {ivs[b]}")
+        snap = {k: v.copy() for k, v in bufs.items()} if isinstance(bufs, dict) else [b.copy() for b in bufs]
+        snap_scratch = {k: v.copy() for k, v in scratch.items()}
+
+        def src_mem(slot, region):
+            if region in (-1, LL_REGION):
+                return snap[slot]
+            if (slot, region) in snap_scratch:
+                return snap_scratch[(slot, region)]
+            return mem(slot, region)
+
         for t in tasks:
             assert t["lo"] % es == 0 and t["hi"] % es == 0
-            if t["vec"]:
+            if t.get("mode") == 2:
+                if not t["dst"]:
+                    continue
+            elif t["vec"]:
                 assert t["lo"] % 16 == 0 and t["hi"] % 16 == 0
             else:
                 assert t["hi"] - t["lo"] < 16
             lo, hi = t["lo"] // es, t["hi"] // es
-            srcs = [mem(s, rg).view(view)[lo:hi] for s, rg in zip(t["src"], t["src_region"])]
+            srcs = [src_mem(s, rg).view(view)[lo:hi] for s, rg in zip(t["src"], t["src_region"])]
             if len(srcs) == 1:
                 out = srcs[0].copy()
             elif dtype == 0:

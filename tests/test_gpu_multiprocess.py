@@ -86,6 +86,40 @@ def _worker(rank, world, port, result_dir):
             dist.barrier()
         dist.barrier()
         ctx.close()
+        # One slot per GPU, small buffers: one-shot (LL) steps, eager chains
+        # and CUDA-graph replays (packets alternate parity regions by epoch).
+        name = {2: "k2_flat", 4: "k4_sock", 8: "k8_sock"}[world]
+        K, progs = golden_programs(name)
+        ctx = executor.Context.from_process_group(K, list(range(K)), 4 << 20)
+        for N, dt in [(1, numeric.BF16), (777, numeric.BF16), (4096, numeric.F32), (30001, numeric.I32)]:
+            es = 2 if dt == numeric.BF16 else 4
+            inputs = numeric.synthetic_inputs(K, N, dt)
+            for _, _, prog, _ in progs[:8]:
+                ctx.write(rank, inputs[rank])
+                plan = ctx.compile(prog, N, dt)
+                if not all(plan.describe()["phase_ll"]):
+                    raise AssertionError(f"expected one-shot steps: {prog.text}")
+                torch.cuda.synchronize()
+                dist.barrier()
+                g = torch.cuda.CUDAGraph()
+                s = torch.cuda.Stream()
+                with torch.cuda.stream(s):
+                    plan.run()  # eager run 1
+                    with torch.cuda.graph(g, stream=s):
+                        plan.run()
+                torch.cuda.synchronize()
+                for _ in range(6):
+                    g.replay()
+                ctx.synchronize()
+                want = [x.copy() for x in inputs]
+                for _ in range(7):
+                    numeric.execute(prog, K, want, dt)
+                if not np.array_equal(ctx.read(rank, N * es), want[rank].view(np.uint8)):
+                    raise AssertionError(f"one-shot replay mismatch rank {rank}: {prog.text} N={N}")
+                del g
+                plan.close()
+                dist.barrier()
+        ctx.close()
         dist.destroy_process_group()
     except Exception:
         ok = False

@@ -224,20 +224,46 @@ def test_two_gpus_config2(mapping, push):
 
 @pytest.mark.multigpu
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("push", [False, True])
-def test_one_slot_per_gpu_small_k(push):
+@pytest.mark.parametrize("push,ll", [(False, False), (True, False), (False, True)])
+def test_one_slot_per_gpu_small_k(push, ll):
     n = min(NGPU, 8)
     name = {2: "k2_flat", 4: "k4_sock", 8: "k8_sock"}.get(n)
     if name is None:
         pytest.skip("GPU count without a golden set")
     ctx = executor.Context.local(n, list(range(n)), max_bytes=64 << 20)
     ctx.set_option("push_min_bytes", 0 if push else -1)
+    ctx.set_option("ll_max_bytes", (256 << 10) if ll else 0)
     try:
         K, progs = golden_programs(name)
         for _, _, prog, _ in progs:
             _run(ctx, prog, K, 4097, numeric.F32)
         for _, _, prog, _ in progs[:4]:
             _run(ctx, prog, K, 16 << 20, numeric.BF16, runs=3)
+    finally:
+        ctx.close()
+
+
+@pytest.mark.multigpu
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_one_shot_steps_repeated():
+    """One-shot (LL) steps: packets alternate between two parity regions by
+    epoch, so many back-to-back runs must chain exactly; ragged sizes exercise
+    the edge packets; every dtype bit-exact. (Graph replay of one-shot steps:
+    test_gpu_multiprocess.py, one process per GPU.)"""
+    n = min(NGPU, 8)
+    name = {2: "k2_flat", 4: "k4_sock", 8: "k8_sock"}.get(n)
+    if name is None:
+        pytest.skip("GPU count without a golden set")
+    ctx = executor.Context.local(n, list(range(n)), max_bytes=8 << 20)
+    try:
+        K, progs = golden_programs(name)
+        for N in (1, 13, 1001, 32 << 10):
+            for dt in (numeric.BF16, numeric.F32, numeric.I32):
+                for _, _, prog, _ in progs[:6]:
+                    plan = ctx.compile(prog, N, dt)
+                    assert all(plan.describe()["phase_ll"])
+                    plan.close()
+                    _run(ctx, prog, K, N, dt, runs=5)
     finally:
         ctx.close()
 

@@ -28,16 +28,18 @@ MAPPINGS = {
 }
 
 
-def _compile(prog, K, mapping, N, dtype, push=False):
+def _compile(prog, K, mapping, N, dtype, push=False, ll=False):
     slot_rank, world = MAPPINGS[mapping](K)
     ctx = executor.Context.virtual(K, slot_rank, world)
     ctx.set_option("push_min_bytes", 0 if push else -1)
+    if world > 1:
+        ctx.set_option("ll_max_bytes", (256 << 10) if ll else 0)
     plan = ctx.compile(prog, N, dtype)
     return ctx, plan, plan.describe()
 
 
-def _check(prog, K, mapping, N, dtype, push=False):
-    ctx, plan, desc = _compile(prog, K, mapping, N, dtype, push)
+def _check(prog, K, mapping, N, dtype, push=False, ll=False):
+    ctx, plan, desc = _compile(prog, K, mapping, N, dtype, push, ll)
     inputs = numeric.synthetic_inputs(K, N, dtype)
     want = [x.copy() for x in inputs]
     numeric.execute(prog, K, want, dtype, nthreads=1)
@@ -226,6 +228,7 @@ def test_nvls_plan_structure_virtual():
     ctx.set_option("push_min_bytes", -1)
     ctx.set_option("nvls", 1)
     ctx.set_option("nvls_min_bytes", 0)
+    ctx.set_option("ll_max_bytes", 0)  # one-shot would take these small steps
     seen = 0
     for _, _, prog, _ in progs[::10]:
         for dtype in (numeric.BF16, numeric.I32):
@@ -244,3 +247,78 @@ def test_nvls_plan_structure_virtual():
             simulate_plan(desc, got, dtype)
             assert all(np.array_equal(a.view(np.uint8), b.view(np.uint8)) for a, b in zip(got, want))
     assert seen > 0
+
+
+# ---- one-shot (LL) steps ----------------------------------------------------
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2_r1", "cfg2_r01", "k8_sock", "k4_flat", "k2_flat"])
+@pytest.mark.parametrize("dtype", [numeric.F32, numeric.BF16, numeric.I32])
+def test_ll_every_program_bit_exact_one_per_gpu(name, dtype):
+    """Small buffers, one slot per GPU: every step is one-shot, the plan is
+    hazard-free, every packet stream has a sender, and the bits equal the
+    oracle's (each destination sums all members in group order)."""
+    K, progs = golden_programs(name)
+    for _, _, prog, _ in progs[:: 3 if name.startswith("cfg2") else 1]:
+        desc = _check(prog, K, "one_per_gpu", 333, dtype, ll=True)
+        assert all(desc["phase_ll"]), prog.text
+        assert desc["final_wait"] == [[] for _ in range(K)]
+        for step in desc["steps"]:
+            for r, rk in enumerate(step["ranks"]):
+                for t in rk["tasks"]:
+                    # no task addresses another GPU's slot buffer directly
+                    assert all(desc["slot_rank"][x] == r for x, rg in zip(t["src"], t["src_region"]) if rg == -1)
+                    assert all(desc["slot_rank"][x] == r for x in t["dst"])
+
+
+@pytest.mark.parametrize("mapping", ["two_gpus", "four_gpus", "interleaved2"])
+@pytest.mark.parametrize("dtype", [numeric.BF16, numeric.I32])
+def test_ll_mixed_mappings(mapping, dtype):
+    """Several slots per GPU: steps whose cross-GPU groups have one member per
+    GPU run one-shot (GPU-local groups as ordinary tasks in the same launch),
+    the others fall back to the pull path; bits equal the oracle's."""
+    rng = random.Random(5)
+    seen = 0
+    for name in ("cfg2_r01", "cfg2_r1", "cfg3_r12", "k8_sock"):
+        K, progs = golden_programs(name)
+        for _, _, prog, _ in rng.sample(progs, min(25, len(progs))):
+            desc = _check(prog, K, mapping, rng.choice([8, 15, 64, 257, 1000, 4099]), dtype, ll=True)
+            seen += sum(desc["phase_ll"])
+    assert seen > 0
+
+
+@pytest.mark.parametrize("N", [0, 1, 5, 9, 31, 127, 4097])
+def test_ll_ragged_sizes(N):
+    K, progs = golden_programs("cfg2_r01")
+    for _, _, prog, _ in progs[::25]:
+        _check(prog, K, "one_per_gpu", N, numeric.BF16, ll=True)
+
+
+def test_ll_budget_selects_variant():
+    """An AllReduce of D bytes over 8 GPUs sends D to each peer: one-shot at
+    D <= ll_max_bytes, pull above it."""
+    K, progs = golden_programs("k8_flat")
+    prog = progs[0][2]
+    ctx = executor.Context.virtual(K, list(range(K)), K)
+    ctx.set_option("push_min_bytes", -1)
+    ctx.set_option("ll_max_bytes", 64 << 10)
+    assert ctx.compile(prog, (64 << 10) // 4, "f32").describe()["phase_ll"] == [1]
+    assert ctx.compile(prog, (64 << 10) // 4 + 2, "f32").describe()["phase_ll"] == [0]
+    ctx.set_option("ll_max_bytes", 0)
+    assert ctx.compile(prog, 16, "f32").describe()["phase_ll"] == [0]
+    ctx.set_option("ll_max_bytes", 1 << 30)  # capped by the reserved area (512 KiB)
+    assert ctx.compile(prog, (1 << 20) // 4, "f32").describe()["phase_ll"] == [0]
+
+
+def test_ll_allreduce_sends_from_inside_the_owner_task():
+    """One-shot AllReduce: each GPU's single task reads its slot, sends it to
+    the 7 peers and sums the 8 packet streams in group order (no separate
+    send tasks, so the value sent is read before it is overwritten)."""
+    K, progs = golden_programs("k8_flat")
+    prog = progs[0][2]
+    _, plan, desc = _compile(prog, K, "one_per_gpu", 1000, numeric.F32, ll=True)
+    for r, rk in enumerate(desc["steps"][0]["ranks"]):
+        assert len(rk["tasks"]) == 1
+        t = rk["tasks"][0]
+        assert t["mode"] == 2 and t["dst"] == [r] and sorted(t["sends"]) == [q for q in range(8) if q != r]
+        assert t["src"] == list(range(8))
+        assert [rg for rg in t["src_region"]] == [-1 if x == r else -3 for x in range(8)]
