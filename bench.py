@@ -390,7 +390,18 @@ def main():
     resc = rescore.topk([{"instance": (tuple(e["request"]), e["matrix"]), "index": e["index"],
                           "sim_seconds": e["prog"].seconds, "measured_us": us, "text": e["prog"].text}
                          for e, us in zip(entries, prog_us)])
-    sim_topk = {"instances": resc["instances"], "top_k": resc["top_k"], "top_k_tie_aware": resc["top_k_tie_aware"]}
+    sim_topk = {"instances": resc["instances"], "top_k": resc["top_k"], "top_k_tie_aware": resc["top_k_tie_aware"],
+                "spearman": resc["spearman"]}
+    # The B200-calibrated model (rs_plan_predict_us) on the same instances:
+    # per launch, measured latency + the plan's own link / HBM bytes at the
+    # measured rates (local launches ~3 us, cross-GPU ~8 us incl. handshake).
+    cal_args = dict(launch_us=3.0, link_gbs=650.0, hbm_gbs=5967.0) if world == 1 else \
+        dict(launch_us=8.0, link_gbs=650.0, hbm_gbs=5967.0)
+    cal = rescore.topk([{"instance": (tuple(e["request"]), e["matrix"]), "index": e["index"],
+                         "sim_seconds": p.predict_us(**cal_args), "measured_us": us, "text": e["prog"].text}
+                        for e, p, us in zip(entries, plans, prog_us)])
+    cal_topk = {"instances": cal["instances"], "top_k": cal["top_k"], "top_k_tie_aware": cal["top_k_tie_aware"],
+                "spearman": cal["spearman"], "model": cal_args}
 
     # End to end through the C-ABI from pinned HOST memory: every step
     # uploads the hosted slots' inputs (rs_ctx_upload), runs the step's
@@ -434,7 +445,8 @@ def main():
     if args.programs_out and rank == 0:
         with open(args.programs_out, "w") as f:
             json.dump([{"request": e["request"], "matrix": e["matrix"], "index": e["index"], "text": e["prog"].text,
-                        "sim_seconds": e["prog"].seconds, "measured_us": us} for e, us in zip(entries, prog_us)], f)
+                        "sim_seconds": e["prog"].seconds, "calibrated_us": p.predict_us(**cal_args), "measured_us": us}
+                       for e, p, us in zip(entries, plans, prog_us)], f)
 
     if rank == 0:
         line = {
@@ -457,6 +469,7 @@ def main():
                            "max": round(max(prog_us), 2)},
             "instances": inst_list,
             "simulator_rescoring": sim_topk,
+            "calibrated_rescoring": cal_topk,
             "speedup_vs_nccl": speedup_vs_nccl,
             "nvls": bool(getattr(ctx, "nvls", False)) if world > 1 else False,
         }

@@ -162,6 +162,15 @@ int rs_plan_launch_count(rs_plan* plan, int* launches);
  * links (link_bytes) and through HBM (hbm_bytes) in step s, maxed over ranks. */
 int rs_plan_step_bytes(rs_plan* plan, int step, double* link_bytes, double* hbm_bytes);
 
+/* B200-calibrated cost of one run, next to the
+ * reference's Simulate (simulator.cc:141-188): per launch phase,
+ * launch_us + max over GPUs of link bytes per direction / link_gbs + max over
+ * GPUs of HBM bytes / hbm_gbs. Unlike the reference model it sees the
+ * executor's actual traffic: per-port non-blocking NVSwitch (no shared-switch
+ * division), local steps at HBM speed, relay fan-out, one-shot and NVLS
+ * variants. Planning-only contexts work (no GPU needed). */
+int rs_plan_predict_us(rs_plan* plan, double launch_us, double link_gbs, double hbm_gbs, double* us);
+
 /* Tuning knobs (0 = default): CTAs per launch cap and threads per CTA. */
 int rs_plan_set_launch(rs_plan* plan, int max_ctas, int threads);
 /* Named knobs: "unroll" (4|8 vectors in flight per thread per source),

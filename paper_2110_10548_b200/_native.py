@@ -32,7 +32,7 @@ EXPORTED_SYMBOLS = (
     "rs_ctx_set_exchange", "rs_ctx_upload", "rs_ctx_download",
     "rs_ctx_destroy", "rs_ctx_buffer", "rs_ctx_local_ranks", "rs_ctx_synchronize",
     "rs_plan_compile", "rs_plan_run", "rs_plan_run_host", "rs_plan_launch_count",
-    "rs_plan_step_bytes", "rs_plan_set_launch", "rs_plan_set_option", "rs_plan_destroy", "rs_plan_time",
+    "rs_plan_step_bytes", "rs_plan_predict_us", "rs_plan_set_launch", "rs_plan_set_option", "rs_plan_destroy", "rs_plan_time",
     "rs_synthesize_json", "rs_report", "rs_run_lowered", "rs_free",
 )
 
@@ -88,6 +88,8 @@ def _declare(lib):
         "rs_plan_run_host": (_I, [_P, _P, _P]),
         "rs_plan_launch_count": (_I, [_P, _PI]),
         "rs_plan_step_bytes": (_I, [_P, _I, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+        "rs_plan_predict_us": (_I, [_P, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                    ctypes.POINTER(ctypes.c_double)]),
         "rs_plan_set_launch": (_I, [_P, _I, _I]),
         "rs_plan_set_option": (_I, [_P, ctypes.c_char_p, ctypes.c_longlong]),
         "rs_plan_destroy": (_I, [_P]),

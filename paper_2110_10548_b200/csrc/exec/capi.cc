@@ -222,6 +222,23 @@ int rs_plan_step_bytes(rs_plan* plan, int step, double* link_bytes, double* hbm_
   return RS_OK;
 }
 
+int rs_plan_predict_us(rs_plan* plan, double launch_us, double link_gbs, double hbm_gbs, double* us) {
+  if (!plan || !us) return Bad("null argument");
+  if (!(link_gbs > 0) || !(hbm_gbs > 0) || launch_us < 0) return Bad("bandwidths must be positive");
+  const rs::Plan* p = plan->impl;
+  double total = 0;
+  for (const std::vector<rs::RankStep>& phase : p->phases) {
+    double link = 0, hbm = 0;
+    for (const rs::RankStep& r : phase) {
+      link = std::max(link, std::max(r.tx_bytes, r.rx_bytes));
+      hbm = std::max(hbm, r.hbm_bytes);
+    }
+    total += launch_us + link / (link_gbs * 1e3) + hbm / (hbm_gbs * 1e3);
+  }
+  *us = total;
+  return RS_OK;
+}
+
 int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value) {
   if (!ctx || !key) return Bad("null argument");
   const std::string k(key);

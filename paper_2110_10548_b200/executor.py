@@ -322,6 +322,15 @@ class Plan:
         nat.check(nat.lib().rs_plan_step_bytes(self._h, step, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value
 
+    def predict_us(self, launch_us: float = 8.0, link_gbs: float = 650.0, hbm_gbs: float = 6000.0) -> float:
+        """B200-calibrated cost of one run from the plan's own traffic
+        (rs_plan_predict_us); defaults = measured per-step latency (K=4),
+        P2P AllReduce link rate and local step kernel HBM rate."""
+        us = ctypes.c_double()
+        nat.check(nat.lib().rs_plan_predict_us(self._h, float(launch_us), float(link_gbs), float(hbm_gbs),
+                                               ctypes.byref(us)))
+        return us.value
+
     def describe(self) -> dict:
         """The compiled plan: per step, per rank, entry-barrier ranks and tasks."""
         import json

@@ -322,3 +322,22 @@ def test_ll_allreduce_sends_from_inside_the_owner_task():
         assert t["mode"] == 2 and t["dst"] == [r] and sorted(t["sends"]) == [q for q in range(8) if q != r]
         assert t["src"] == list(range(8))
         assert [rg for rg in t["src_region"]] == [-1 if x == r else -3 for x in range(8)]
+
+
+def test_calibrated_cost_model():
+    """rs_plan_predict_us: per launch, latency + the plan's own max link bytes
+    / link rate + max HBM bytes / HBM rate."""
+    K, progs = golden_programs("k8_flat")
+    prog = progs[0][2]  # single AllReduce over 8 GPUs
+    N = 1 << 24  # f32, 64 MiB per GPU
+    _, plan, desc = _compile(prog, K, "one_per_gpu", N, numeric.F32)
+    link, hbm = plan.step_bytes(0)
+    us = plan.predict_us(launch_us=8.0, link_gbs=650.0, hbm_gbs=6000.0)
+    assert abs(us - (8.0 + link / 650e3 + hbm / 6000e3)) < 1e-6
+    assert abs(link - 2 * 7 / 8 * N * 4) <= 64
+    # one GPU: no link bytes, the HBM term only
+    _, plan1, _ = _compile(prog, K, "local", N, numeric.F32)
+    l1, h1 = plan1.step_bytes(0)
+    assert l1 == 0 and abs(plan1.predict_us(3.0, 650.0, 6000.0) - (3.0 + h1 / 6000e3)) < 1e-6
+    with pytest.raises(ExecError):
+        plan.predict_us(8.0, 0.0, 6000.0)
