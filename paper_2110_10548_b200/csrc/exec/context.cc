@@ -434,7 +434,7 @@ absl::Status EnsureMulticast(Context* ctx, const std::vector<int>& slots, int* i
     drv::cuDeviceGet(&dev, ctx->ranks[r].ordinal);
     return dev;
   };
-  auto bind_and_map = [&](int r, int slot, const std::vector<int>& access) -> absl::Status {
+  auto bind = [&](int r, int slot) -> absl::Status {
     RS_CUDA(cudaSetDevice(ctx->ranks[r].ordinal));
     absl::Status s = CuStatus(
         drv::cuMulticastBindMem(mc->handle, 0, ctx->ranks[r].vmm.handle, ctx->SlotOffset(slot, -1), mc->bytes, 0),
@@ -468,7 +468,7 @@ absl::Status EnsureMulticast(Context* ctx, const std::vector<int>& slots, int* i
       access.push_back(ctx->ranks[r].ordinal);
     }
     for (int d : slots) {
-      s = bind_and_map(ctx->slot_rank[d], d, access);
+      s = bind(ctx->slot_rank[d], d);
       if (!s.ok()) return s;
     }
     CUdeviceptr va = 0;
@@ -537,7 +537,7 @@ absl::Status EnsureMulticast(Context* ctx, const std::vector<int>& slots, int* i
     }
     int32_t bound = 1;
     if (member) {
-      s = bind_and_map(me, my_slot, {ctx->ranks[me].ordinal});
+      s = bind(me, my_slot);
       if (s.ok()) s = map_va({ctx->ranks[me].ordinal}, &mc->va[me]);
       bound = s.ok() ? 1 : 0;
     }

@@ -169,6 +169,8 @@ class Plan {
   std::vector<uint8_t> phase_ll;              // 1: one-shot (LL) phase
   std::vector<uint8_t> final_wait_bits;       // per rank: ranks for the tail wait
   // Device copies (per driven rank): all tasks / pointer tables of all phases.
+  std::vector<StepArgs> launch_args;  // [phase * world + rank], built with ctas_per_sm
+  std::vector<int> launch_grid;
   std::vector<Task*> d_tasks;
   std::vector<void**> d_ptrs;
   std::vector<std::vector<size_t>> task_offset, ptr_offset;  // [rank][phase]

@@ -850,6 +850,58 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
   return absl::OkStatus();
 }
 
+// Launch records of every (phase, driven rank), built once per launch shape
+// (the per-run host path is then one launch per record).
+void BuildLaunches(Plan* plan) {
+  Context* ctx = plan->ctx;
+  const int P = plan->num_phases();
+  const int R = ctx->world;
+  plan->launch_args.assign(static_cast<size_t>(P) * R, StepArgs{});
+  plan->launch_grid.assign(static_cast<size_t>(P) * R, 1);
+  for (int ph = 0; ph < P; ++ph) {
+    for (int r : ctx->DrivenRanks()) {
+      const Rank& rank = ctx->ranks[r];
+      const RankStep& rsx = plan->phases[ph][r];
+      StepArgs& a = plan->launch_args[static_cast<size_t>(ph) * R + r];
+      a.tasks = plan->d_tasks[r] ? plan->d_tasks[r] + plan->task_offset[r][ph] : nullptr;
+      a.ptrs = plan->d_ptrs[r] ? plan->d_ptrs[r] + plan->ptr_offset[r][ph] : nullptr;
+      a.ntasks = static_cast<uint32_t>(rsx.tasks.size());
+      a.npieces = rsx.npieces;
+      a.piece_bytes = rsx.piece_bytes;
+      a.dtype = plan->dtype;
+      a.arrive_counter = reinterpret_cast<unsigned int*>(rank.heap + kCounterOffset);
+      a.error_flag = reinterpret_cast<int*>(rank.heap + kErrorOffset);
+      a.inbox = reinterpret_cast<const uint64_t*>(rank.heap + kInboxOffset);
+      a.timeout_ns = ctx->timeout_ns;
+      a.ll_parity_stride = ctx->LLRegionBytes();
+      if (ctx->world > 1) {
+        for (int q = 0; q < ctx->world; ++q) {
+          if (q == r) continue;
+          a.signal_ptrs[a.nsignal++] = reinterpret_cast<uint64_t*>(rank.view[q] + kInboxOffset) + r;
+        }
+        for (uint8_t q : rsx.wait) a.wait_ranks[a.nwait++] = q;
+        if (ph == P - 1) {
+          for (int q = 0; q < ctx->world; ++q)
+            if (plan->final_wait_bits[r] & (1u << q)) a.final_ranks[a.nfinal++] = static_cast<uint8_t>(q);
+        }
+      }
+      a.signal_done = rsx.signal_done ? 1u : 0u;
+      a.epoch_base = reinterpret_cast<uint64_t*>(rank.heap + kEpochOffset);
+      a.step = static_cast<uint32_t>(ph);
+      a.num_steps = static_cast<uint32_t>(P);
+      for (const Task& t : rsx.tasks) {
+        a.has_nvls |= t.mode == kModeNvlsAllReduce ? 1u : 0u;
+        a.has_ll |= t.mode == kModeLL ? 1u : 0u;
+      }
+      const int resident = plan->ctas_per_sm * rank.sm_count;
+      int cap = plan->max_ctas > 0 ? std::min(plan->max_ctas, resident) : resident;
+      if (rsx.max_grid > 0) cap = std::min<int>(cap, static_cast<int>(rsx.max_grid));
+      if (cap <= 0) cap = 148;
+      plan->launch_grid[static_cast<size_t>(ph) * R + r] = std::max(1, std::min<int>(cap, static_cast<int>(rsx.npieces)));
+    }
+  }
+}
+
 absl::Status RunPlan(Plan* plan, void* const* device_bufs, void* const* host_bufs,
                      void* const* streams) {
   Context* ctx = plan->ctx;
@@ -887,51 +939,24 @@ absl::Status RunPlan(Plan* plan, void* const* device_bufs, void* const* host_buf
     absl::Status st = CudaStatus(cudaSetDevice(ctx->ranks[driven[0]].ordinal), "cudaSetDevice");
     if (!st.ok()) return st;
     plan->ctas_per_sm = MaxResidentCtas(plan->dtype, plan->threads, plan->unroll);
+    BuildLaunches(plan);
+  }
+  const int R = ctx->world;
+  if (driven.size() == 1) {
+    absl::Status st = CudaStatus(cudaSetDevice(ctx->ranks[driven[0]].ordinal), "cudaSetDevice");
+    if (!st.ok()) return st;
   }
   for (int ph = 0; ph < P; ++ph) {
     for (size_t i = 0; i < driven.size(); ++i) {
       const int r = driven[i];
-      const Rank& rank = ctx->ranks[r];
-      const RankStep& rsx = plan->phases[ph][r];
-      StepArgs a{};
-      a.tasks = plan->d_tasks[r] ? plan->d_tasks[r] + plan->task_offset[r][ph] : nullptr;
-      a.ptrs = plan->d_ptrs[r] ? plan->d_ptrs[r] + plan->ptr_offset[r][ph] : nullptr;
-      a.ntasks = static_cast<uint32_t>(rsx.tasks.size());
-      a.npieces = rsx.npieces;
-      a.piece_bytes = rsx.piece_bytes;
-      a.dtype = plan->dtype;
-      a.arrive_counter = reinterpret_cast<unsigned int*>(rank.heap + kCounterOffset);
-      a.error_flag = reinterpret_cast<int*>(rank.heap + kErrorOffset);
-      a.inbox = reinterpret_cast<const uint64_t*>(rank.heap + kInboxOffset);
-      a.timeout_ns = ctx->timeout_ns;
-      a.ll_parity_stride = ctx->LLRegionBytes();
-      if (ctx->world > 1) {
-        for (int q = 0; q < ctx->world; ++q) {
-          if (q == r) continue;
-          a.signal_ptrs[a.nsignal++] = reinterpret_cast<uint64_t*>(rank.view[q] + kInboxOffset) + r;
-        }
-        for (uint8_t q : rsx.wait) a.wait_ranks[a.nwait++] = q;
-        if (ph == P - 1) {
-          for (int q = 0; q < ctx->world; ++q)
-            if (plan->final_wait_bits[r] & (1u << q)) a.final_ranks[a.nfinal++] = static_cast<uint8_t>(q);
-        }
+      if (driven.size() > 1) {
+        absl::Status st = CudaStatus(cudaSetDevice(ctx->ranks[r].ordinal), "cudaSetDevice");
+        if (!st.ok()) return st;
       }
-      a.signal_done = rsx.signal_done ? 1u : 0u;
-      a.epoch_base = reinterpret_cast<uint64_t*>(rank.heap + kEpochOffset);
-      a.step = static_cast<uint32_t>(ph);
-      a.num_steps = static_cast<uint32_t>(P);
-      for (const Task& t : rsx.tasks) {
-        a.has_nvls |= t.mode == kModeNvlsAllReduce ? 1u : 0u;
-        a.has_ll |= t.mode == kModeLL ? 1u : 0u;
-      }
-      const int resident = plan->ctas_per_sm * rank.sm_count;
-      int cap = plan->max_ctas > 0 ? std::min(plan->max_ctas, resident) : resident;
-      if (rsx.max_grid > 0) cap = std::min<int>(cap, static_cast<int>(rsx.max_grid));
-      if (cap <= 0) cap = 148;
-      const int grid = std::max(1, std::min<int>(cap, static_cast<int>(rsx.npieces)));
-      absl::Status st = CudaStatus(cudaSetDevice(rank.ordinal), "cudaSetDevice");
-      if (!st.ok()) return st;
-      st = CudaStatus(LaunchStep(a, grid, plan->threads, plan->unroll, stream_of(i)), "step kernel launch");
+      const size_t k = static_cast<size_t>(ph) * R + r;
+      absl::Status st = CudaStatus(
+          LaunchStep(plan->launch_args[k], plan->launch_grid[k], plan->threads, plan->unroll, stream_of(i)),
+          "step kernel launch");
       if (!st.ok()) return st;
     }
   }

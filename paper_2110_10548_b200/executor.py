@@ -98,6 +98,18 @@ def _stream_handle(stream) -> int:
     return h if h else _CUDA_STREAM_LEGACY
 
 
+def _current_stream_handle(ordinal: int) -> int:
+    """Raw handle of torch's current stream on `ordinal` (the fast path of
+    torch.cuda.current_stream(o).cuda_stream; per-run host overhead matters
+    for small programs)."""
+    import torch
+    try:
+        h = torch._C._cuda_getCurrentRawStream(ordinal)
+    except AttributeError:  # pragma: no cover - older torch
+        h = torch.cuda.current_stream(ordinal).cuda_stream
+    return h if h else _CUDA_STREAM_LEGACY
+
+
 class Context:
     """Owns the per-GPU heaps (slot buffers + barrier flags) of K slots."""
 
@@ -269,6 +281,9 @@ class Plan:
                                             mem.ctypes.data_as(p32), self.elems, self.dtype,
                                             ctypes.byref(h)))
         self._h = h
+        self._run_fn = nat.lib().rs_plan_run
+        self._stream_key = None
+        self._stream_arr = None
 
     def close(self):
         if self._h:
@@ -283,10 +298,13 @@ class Plan:
 
     def _streams(self, streams):
         if streams is None:
-            import torch
-            streams = [_stream_handle(torch.cuda.current_stream(o)) for o in self.ctx.local_ordinals]
-        arr = (ctypes.c_void_p * max(1, len(streams)))(*[ctypes.c_void_p(s) for s in streams])
-        return arr
+            key = tuple(_current_stream_handle(o) for o in self.ctx.local_ordinals)
+        else:
+            key = tuple(streams)
+        if key != self._stream_key:  # cached: the common case is the same stream every run
+            self._stream_arr = (ctypes.c_void_p * max(1, len(key)))(*[ctypes.c_void_p(s) for s in key])
+            self._stream_key = key
+        return self._stream_arr
 
     def run(self, bufs=None, streams=None):
         """Enqueue. bufs=None: in place on the context buffers; else K device
@@ -295,7 +313,9 @@ class Plan:
         if bufs is not None:
             ptrs = [b if isinstance(b, int) else (b.data_ptr() if b is not None else 0) for b in bufs]
             arr = (ctypes.c_void_p * self.ctx.K)(*[ctypes.c_void_p(p) for p in ptrs])
-        nat.check(nat.lib().rs_plan_run(self._h, arr, self._streams(streams)))
+        code = self._run_fn(self._h, arr, self._streams(streams))
+        if code:
+            nat.check(code)
 
     def run_host(self, host_bufs, streams=None):
         """End to end from host memory: H2D copy-in, program, D2H copy-out."""

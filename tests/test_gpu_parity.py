@@ -268,6 +268,41 @@ def test_one_shot_steps_repeated():
         ctx.close()
 
 
+@pytest.mark.multigpu
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("ll", [False, True])
+def test_config3_programs_across_gpus(ll):
+    """Config 3 (axes [2,2,2], every one- and two-axis request) with the 8
+    slots block-distributed over the GPUs; one-shot steps on or off."""
+    n = min(NGPU, 4)
+    ctx = executor.Context.local(8, [d * n // 8 for d in range(8)], max_bytes=8 << 20)
+    ctx.set_option("ll_max_bytes", (256 << 10) if ll else 0)
+    try:
+        for name in ("cfg3_r0", "cfg3_r1", "cfg3_r2", "cfg3_r01", "cfg3_r02", "cfg3_r12"):
+            K, progs = golden_programs(name)
+            for _, _, prog, _ in progs[::9]:
+                _run(ctx, prog, K, 1001, numeric.F32)
+                _run(ctx, prog, K, 777, numeric.I32, runs=2)
+    finally:
+        ctx.close()
+
+
+@pytest.mark.multigpu
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_config1_full_size_across_gpus():
+    """Config 1 at its full size (64 MiB f32 per device) on 2 or 4 GPUs."""
+    n = min(NGPU, 4)
+    ctx = executor.Context.local(8, [d * n // 8 for d in range(8)], max_bytes=64 << 20)
+    try:
+        K, progs = golden_programs("cfg1")
+        N = 16 * 1024 * 1024
+        inputs = numeric.synthetic_inputs(K, N, numeric.F32)
+        for _, _, prog, _ in progs:
+            _run(ctx, prog, K, N, numeric.F32, inputs=inputs)
+    finally:
+        ctx.close()
+
+
 def test_cpp_host_example_end_to_end():
     """C++ host: reference planner API -> redsynth::GpuExecutor::Execute on
     every config-2 (reduce {0,1}) program, int32 identity checked in C++."""
