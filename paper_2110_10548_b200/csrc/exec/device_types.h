@@ -55,6 +55,7 @@ struct StepArgs {
   uint32_t has_nvls;  // any multimem task: order unicast/multicast aliases (fence.proxy.alias)
   uint32_t has_ll;    // any one-shot task: launch the LL instantiation
   uint32_t signal_done;  // some peer waits for this step's epoch (else no exit fence)
+  uint32_t wait_lag;     // entry waits for base + step - wait_lag (one-shot after one-shot: 1)
   uint8_t wait_ranks[RS_MAX_RANKS];
   uint8_t final_ranks[RS_MAX_RANKS];
   // Epochs are relative to a device-resident run base (so a captured CUDA

@@ -167,6 +167,7 @@ class Plan {
   std::vector<std::vector<RankStep>> phases;  // [phase][rank]
   std::vector<int> phase_step;                // program step of each phase
   std::vector<uint8_t> phase_ll;              // 1: one-shot (LL) phase
+  std::vector<uint8_t> phase_lag;             // 1: entry waits one epoch less (LL after LL)
   std::vector<uint8_t> final_wait_bits;       // per rank: ranks for the tail wait
   // Device copies (per driven rank): all tasks / pointer tables of all phases.
   std::vector<StepArgs> launch_args;  // [phase * world + rank], built with ctas_per_sm

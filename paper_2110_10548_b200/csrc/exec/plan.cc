@@ -797,19 +797,29 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
     }
   }
 
+  // A one-shot phase right after another one-shot phase waits one epoch
+  // less: nobody wrote or reads its ranks' slots remotely in the previous
+  // phase, so it only has to know that its receivers consumed the packets
+  // of two phases ago (same parity region), i.e. finished phase t-2.
+  plan->phase_lag.assign(P, 0);
+  for (int ph = 1; ph < P; ++ph) plan->phase_lag[ph] = plan->phase_ll[ph] && plan->phase_ll[ph - 1] ? 1 : 0;
   // End-of-phase epochs nobody waits for are not published (the exit fence
-  // is most of a small step's cost): phase ph's epoch is awaited by the next
-  // phase's entry sets, or, for the last phase, by the tail waits.
+  // is most of a small step's cost): phase ph's epoch is awaited by phase
+  // ph+1 (lag 0) or ph+2 (lag 1) entry sets, or, for the last phase, by the
+  // tail waits.
   for (int ph = 0; ph < P; ++ph) {
     for (int r = 0; r < R; ++r) {
-      bool needed = false;
-      for (int q = 0; q < R && !needed; ++q) {
-        if (q == r) continue;
-        if (ph + 1 < P) {
-          const std::vector<uint8_t>& w = plan->phases[ph + 1][q].wait;
+      bool needed = ph + 1 == P && [&] {
+        for (int q = 0; q < R; ++q)
+          if (q != r && ((plan->final_wait_bits[q] >> r) & 1u)) return true;
+        return false;
+      }();
+      for (int t = ph + 1; t < P && t <= ph + 2 && !needed; ++t) {
+        if (t - plan->phase_lag[t] - 1 != ph) continue;
+        for (int q = 0; q < R && !needed; ++q) {
+          if (q == r) continue;
+          const std::vector<uint8_t>& w = plan->phases[t][q].wait;
           needed = std::find(w.begin(), w.end(), static_cast<uint8_t>(r)) != w.end();
-        } else {
-          needed = (plan->final_wait_bits[q] >> r) & 1u;
         }
       }
       plan->phases[ph][r].signal_done = needed;
@@ -886,6 +896,7 @@ void BuildLaunches(Plan* plan) {
         }
       }
       a.signal_done = rsx.signal_done ? 1u : 0u;
+      a.wait_lag = static_cast<uint32_t>(plan->phase_lag[ph]);
       a.epoch_base = reinterpret_cast<uint64_t*>(rank.heap + kEpochOffset);
       a.step = static_cast<uint32_t>(ph);
       a.num_steps = static_cast<uint32_t>(P);
@@ -970,6 +981,7 @@ std::string DescribePlan(const Plan& plan) {
   doc["num_phases"] = plan.num_phases();
   doc["phase_step"] = plan.phase_step;
   doc["phase_ll"] = plan.phase_ll;
+  doc["phase_lag"] = plan.phase_lag;
   doc["bytes"] = plan.bytes;
   doc["world"] = plan.ctx->world;
   doc["slot_rank"] = plan.ctx->slot_rank;

@@ -448,12 +448,9 @@ __device__ __forceinline__ void LLReceive(const Task& t, void* const* ptrs, uint
   }
 }
 
-// kLL: the phase holds one-shot tasks (a separate instantiation keeps the
-// packet code out of the bulk kernels' register allocation).
+// One launch phase of one rank: entry barrier, tasks, exit.
 template <int DT, int kUnroll, bool kLL>
-__global__ void __launch_bounds__(512, kUnroll == 4 ? 2 : 1) StepKernel(const __grid_constant__ StepArgs a) {
-  // Run base epoch (device resident; advanced by the previous run's last step).
-  const uint64_t base = a.nsignal ? *reinterpret_cast<volatile uint64_t*>(a.epoch_base) : 0;
+__device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
   // 1. First step of a run: publish "my inputs are in place" to every peer.
   if (a.step == 0 && blockIdx.x == 0 && threadIdx.x < a.nsignal) {
     // Inputs were written by earlier stream work (complete at kernel
@@ -464,7 +461,7 @@ __global__ void __launch_bounds__(512, kUnroll == 4 ? 2 : 1) StepKernel(const __
   // 2. Entry barrier: the ranks whose buffers this step touches (and whose
   //    previous-step writers) have finished the previous step.
   if (threadIdx.x < a.nwait) {
-    WaitAtLeast(a.inbox + a.wait_ranks[threadIdx.x], base + a.step, a.timeout_ns, a.error_flag);
+    WaitAtLeast(a.inbox + a.wait_ranks[threadIdx.x], base + a.step - a.wait_lag, a.timeout_ns, a.error_flag);
   }
   __syncthreads();
   if (a.has_nvls) FenceProxyAlias();
@@ -518,13 +515,13 @@ __global__ void __launch_bounds__(512, kUnroll == 4 ? 2 : 1) StepKernel(const __
   // 4. Exit: the last CTA to finish publishes the step's epoch to all ranks
   //    (skipped when no peer waits for it, e.g. after a one-shot last step).
   const bool last_step = a.step + 1 == a.num_steps;
-  if (a.nsignal == 0) return;  // one GPU: no epochs
-  if (!a.signal_done && !last_step) return;
-  // The CTA barrier orders every thread's stores before thread 0's system
-  // fence (cumulativity); one fence per CTA instead of one per thread.
+  const bool publish = a.signal_done && a.nsignal > 0;
+  const bool advance = last_step && a.nsignal > 0;
+  if (!publish && !advance) return;
+  // The CTA barrier orders every thread's stores before thread 0's fence
+  // (cumulativity); one fence per CTA instead of one per thread.
   __syncthreads();
   if (threadIdx.x == 0) {
-    const bool publish = a.signal_done;
     if (publish) {
       if (a.has_nvls) FenceProxyAlias();
       FenceSys();
@@ -536,9 +533,9 @@ __global__ void __launch_bounds__(512, kUnroll == 4 ? 2 : 1) StepKernel(const __
         if (RS_SYNC_STRICT || gridDim.x > 1) FenceSys();  // acquire the other CTAs' releases
         for (uint32_t q = 0; q < a.nsignal; ++q) SignalStore(a.signal_ptrs[q], base + a.step + 1);
       }
-      // 5. Last step: the run is complete here only once every rank that
-      //    writes into our slots has finished too; then advance the base.
       if (last_step) {
+        // 5. Last step: the run is complete here only once every rank that
+        //    writes into our slots has finished too; then advance the base.
         for (uint32_t i = 0; i < a.nfinal; ++i) {
           WaitAtLeast(a.inbox + a.final_ranks[i], base + a.num_steps, a.timeout_ns, a.error_flag);
         }
@@ -546,6 +543,13 @@ __global__ void __launch_bounds__(512, kUnroll == 4 ? 2 : 1) StepKernel(const __
       }
     }
   }
+}
+
+template <int DT, int kUnroll, bool kLL>
+__global__ void __launch_bounds__(512, kUnroll == 4 ? 2 : 1) StepKernel(const __grid_constant__ StepArgs a) {
+  // Run base epoch (device resident; advanced by the previous run's last step).
+  const uint64_t base = a.nsignal ? *reinterpret_cast<volatile uint64_t*>(a.epoch_base) : 0;
+  Phase<DT, kUnroll, kLL>(a, base);
 }
 
 template <int U>

@@ -262,6 +262,10 @@ def test_ll_every_program_bit_exact_one_per_gpu(name, dtype):
         desc = _check(prog, K, "one_per_gpu", 333, dtype, ll=True)
         assert all(desc["phase_ll"]), prog.text
         assert desc["final_wait"] == [[] for _ in range(K)]
+        # one-shot after one-shot waits one epoch less; the last phase's
+        # epoch is never awaited
+        assert desc["phase_lag"] == [0] + [1] * (desc["num_phases"] - 1)
+        assert not any(rk["signal"] for rk in desc["steps"][-1]["ranks"])
         for step in desc["steps"]:
             for r, rk in enumerate(step["ranks"]):
                 for t in rk["tasks"]:
