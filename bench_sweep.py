@@ -36,7 +36,10 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--graph", action="store_true",
                     help="time `iters` back-to-back ops captured in one CUDA graph (both arms)")
+    ap.add_argument("--no-nvls", action="store_true", help="P2P kernels only (bit-exact everywhere)")
     args = ap.parse_args()
+    if not args.no_nvls:
+        os.environ.setdefault("RS_NVLS", "1")  # AllReduce groups of >= 4 GPUs at >= 16 MiB
 
     import torch
     import torch.distributed as dist
