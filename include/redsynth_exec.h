@@ -115,7 +115,8 @@ int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value);
  * run as multimem.ld_reduce + multimem.st through the NVSwitch. The switch
  * sums in its own order, so f32/bf16 results match the ordered oracle within
  * tolerance instead of bit for bit (i32 never uses NVLS). Options "nvls"
- * (0/1) and "nvls_min_group" tune later compiles. */
+ * (0/1), "nvls_min_group" and "nvls_min_bytes" (default 256 MiB for groups
+ * of < 8 GPUs, 16 MiB for >= 8; env RS_NVLS_MIN_BYTES) tune later compiles. */
 int rs_ctx_nvls(rs_ctx* ctx, int* enabled);
 /* Host all-gather used to set up multicast objects collectively in the
  * one-process-per-GPU mode: fn(send, bytes, recv[world * bytes], user) must

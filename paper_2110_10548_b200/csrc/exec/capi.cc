@@ -257,6 +257,7 @@ int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value) {
     ctx->impl->nvls_min_group = static_cast<int>(value);
   } else if (k == "nvls_min_bytes") {
     ctx->impl->nvls_min_bytes = value < 0 ? ~0ull : static_cast<uint64_t>(value);
+    ctx->impl->nvls_min_bytes_n8 = ctx->impl->nvls_min_bytes;
   } else if (k == "ll_max_bytes") {
     ctx->impl->ll_max_bytes = value < 0 ? 0 : static_cast<uint64_t>(value);
   } else {

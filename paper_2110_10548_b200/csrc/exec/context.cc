@@ -126,7 +126,10 @@ void DecideNvls(Context* ctx, const std::vector<int>& ordinals) {
   ctx->use_vmm = true;
   ctx->nvls = true;
   if (const char* g = std::getenv("RS_NVLS_MIN_GROUP")) ctx->nvls_min_group = std::max(2, std::atoi(g));
-  if (const char* b = std::getenv("RS_NVLS_MIN_BYTES")) ctx->nvls_min_bytes = std::strtoull(b, nullptr, 10);
+  if (const char* b = std::getenv("RS_NVLS_MIN_BYTES")) {
+    ctx->nvls_min_bytes = std::strtoull(b, nullptr, 10);
+    ctx->nvls_min_bytes_n8 = ctx->nvls_min_bytes;
+  }
 }
 
 void ReadTimeoutEnv(Context* ctx) {

@@ -104,9 +104,13 @@ class Context {
   bool use_vmm = false;
   bool nvls = false;
   int nvls_min_group = 4;
-  // Below this many bytes per group the P2P kernel's lower latency wins
-  // (measured crossover ~16 MiB at n = 4, profiles/r01_sweep_n4_bf16_graph_nvls.json).
-  uint64_t nvls_min_bytes = 16ull << 20;
+  // Below this many bytes per group the P2P kernel wins: at n = 4 P2P is
+  // faster up to 128 MiB and NVLS from 256 MiB (1 CTA per SM for multi-peer
+  // pulls; profiles/r01_sweep_n4_nvls_vs_p2p.txt). Groups of >= 8 GPUs move
+  // 1.75 c per GPU with P2P vs 1.125 c with NVLS (1.5 vs 1.25 at n = 4), so
+  // they switch earlier (nvls_min_bytes_n8; not measured: no 8-GPU box).
+  uint64_t nvls_min_bytes = 256ull << 20;
+  uint64_t nvls_min_bytes_n8 = 16ull << 20;
   // One-shot (LL) steps: when every cross-GPU group of a step has its members
   // on distinct GPUs and each GPU sends any peer at most ll_max_bytes, the
   // step runs as one kernel in which every owner receives its sources as
@@ -146,6 +150,7 @@ struct RankStep {
   uint32_t npieces = 0;
   uint32_t piece_bytes = kPieceBytes;  // 4 KiB .. 64 KiB, sized to fill the GPU
   uint32_t max_grid = 0;      // 0 = resident capacity (one-shot phases: a few CTAs)
+  int remote_peers = 0;       // distinct peer GPUs the tasks address
   std::vector<uint8_t> wait;  // ranks to wait for before the phase
   bool signal_done = true;    // a peer waits for this rank's end-of-phase epoch
   double tx_bytes = 0, rx_bytes = 0, hbm_bytes = 0;

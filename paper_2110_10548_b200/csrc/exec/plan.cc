@@ -237,7 +237,8 @@ struct Compiler {
   // NVLS applies to AllReduce groups of >= nvls_min_group slots, one per GPU,
   // for floating-point data.
   bool NvlsEligible(const std::vector<int>& g, uint64_t bytes) const {
-    if (!ctx->nvls || dtype == RS_I32 || bytes == 0 || bytes < ctx->nvls_min_bytes) return false;
+    const uint64_t min_bytes = g.size() >= 8 ? ctx->nvls_min_bytes_n8 : ctx->nvls_min_bytes;
+    if (!ctx->nvls || dtype == RS_I32 || bytes == 0 || bytes < min_bytes) return false;
     if (static_cast<int>(g.size()) < ctx->nvls_min_group) return false;
     if (ctx->mc_groups.size() >= kMaxMcGroups && !ctx->mc_groups.count(g)) return false;
     std::vector<int> ranks;
@@ -765,6 +766,19 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
     }
   }
 
+  // Distinct peer GPUs each rank's tasks address per phase (launch shape).
+  for (std::vector<RankStep>& phase : plan->phases) {
+    for (int r = 0; r < R; ++r) {
+      std::set<int> peers;
+      for (const Ref& ref : phase[r].ptr_refs) {
+        if (ref.region == kMcRegion) continue;
+        const int q = ref.region == kLLRegion ? ref.ll_recv : ctx->slot_rank[ref.slot];
+        if (q != r) peers.insert(q);
+      }
+      phase[r].remote_peers = static_cast<int>(peers.size());
+    }
+  }
+
   // 4. Barrier sets (phases of one step share its groups).
   const int P = plan->num_phases();
   auto group_of = [&](int ph, int d) -> std::vector<int> {
@@ -907,6 +921,11 @@ void BuildLaunches(Plan* plan) {
       const int resident = plan->ctas_per_sm * rank.sm_count;
       int cap = plan->max_ctas > 0 ? std::min(plan->max_ctas, resident) : resident;
       if (rsx.max_grid > 0) cap = std::min<int>(cap, static_cast<int>(rsx.max_grid));
+      // Pulling from >= 2 peers at once: one CTA per SM keeps fewer loads in
+      // flight and measured +6 % at K=4 (637 vs 597 GB/s bus, 256 MiB
+      // AllReduce, profiles/r01_tune4_push0.log); from one peer two per SM
+      // are better (652 vs 637 at K=2, r01_tune_n2.log).
+      if (plan->max_ctas == 0 && !a.has_nvls && !a.has_ll && rsx.remote_peers >= 2) cap = std::min(cap, rank.sm_count);
       if (cap <= 0) cap = 148;
       plan->launch_grid[static_cast<size_t>(ph) * R + r] = std::max(1, std::min<int>(cap, static_cast<int>(rsx.npieces)));
     }
