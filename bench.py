@@ -367,10 +367,22 @@ def main():
         else:  # several slots per GPU: the plan's own per-GPU link bytes
             alg = sum(p.step_bytes(s)[0] for p in plans for s in range(p.program.num_steps))
         achieved = alg / (ms_per_step * 1e-3) / 1e9
+        traffic, tnote = None, "no NVLink capture found"
+        try:  # committed ncu capture of the cross-GPU kernel (tools/profile_p2p.py, profiles/)
+            with open(os.path.join(ROOT, "profiles", "r01_ncu_nvlink.json")) as f:
+                caps = json.load(f)
+            cap = caps.get(f"k{min(world, 4)}_p2p") or next(iter(caps.values()))
+            traffic = cap["nvlrx_user"] + cap["nvltx_user"]
+            tnote = (f"traffic = NVLink user bytes rx+tx of one profiled launch ({cap['what']}, replayed alone), "
+                     f"{traffic / (2 * cap['own_share_algorithmic']):.4f} x its algorithmic bytes; link protocol "
+                     f"overhead on top: rx +{cap['nvlrx_total'] / cap['nvlrx_user'] - 1:.0%}, "
+                     f"tx +{cap['nvltx_total'] / cap['nvltx_user'] - 1:.0%} (profiles/r01_ncu_nvlink.txt)")
+        except Exception:
+            pass
         roofline = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
-                    "frac": round(achieved / NVLINK_PEAK_GBS, 4), "traffic": None,
+                    "frac": round(achieved / NVLINK_PEAK_GBS, 4), "traffic": traffic,
                     "note": "per-GPU per-direction link bytes of SURVEY §8(d) (T_roof = sum_s max_g f*c_g) "
-                            "over the measured step; peak = measured peer copy 770 GB/s (900 nominal)"}
+                            "over the measured step; peak = measured peer copy 770 GB/s (900 nominal); " + tnote}
 
     # per (request, placement): baseline AllReduce and best synthesized program
     instances = {}

@@ -878,6 +878,8 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
 // (the per-run host path is then one launch per record).
 void BuildLaunches(Plan* plan) {
   Context* ctx = plan->ctx;
+  const char* solo_env = std::getenv("RS_SOLO_PROFILE");
+  const bool solo = solo_env && std::atoi(solo_env) != 0;
   const int P = plan->num_phases();
   const int R = ctx->world;
   plan->launch_args.assign(static_cast<size_t>(P) * R, StepArgs{});
@@ -908,6 +910,13 @@ void BuildLaunches(Plan* plan) {
           for (int q = 0; q < ctx->world; ++q)
             if (plan->final_wait_bits[r] & (1u << q)) a.final_ranks[a.nfinal++] = static_cast<uint8_t>(q);
         }
+      }
+      if (solo) {
+        // Profiling aid (RS_SOLO_PROFILE=1): no cross-GPU waits, so ncu can
+        // replay one GPU's pull/push kernel alone and count its NVLink bytes
+        // (results are garbage; never set in production).
+        a.nwait = 0;
+        a.nfinal = 0;
       }
       a.signal_done = rsx.signal_done ? 1u : 0u;
       a.wait_lag = static_cast<uint32_t>(plan->phase_lag[ph]);

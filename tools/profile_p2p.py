@@ -1,0 +1,50 @@
+#!/usr/bin/env python
+"""ncu driver for the cross-GPU step kernel (one process, K GPUs, one slot
+per GPU): with RS_SOLO_PROFILE=1 the kernels skip their cross-GPU waits, so
+ncu (which serialises launches) can replay each GPU's kernel alone and count
+its NVLink bytes (nvltx/nvlrx) next to its DRAM bytes. The data is garbage in
+this mode — it only measures traffic.
+
+  RS_SOLO_PROFILE=1 ncu --metrics gpu__time_duration.sum,nvltx__bytes.sum,nvlrx__bytes.sum,\
+dram__bytes_read.sum,dram__bytes_write.sum python tools/profile_p2p.py --gpus 2
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=2)
+    ap.add_argument("--mib", type=int, default=256)
+    ap.add_argument("--program", type=int, default=0)
+    ap.add_argument("--dtype", default="bf16")
+    args = ap.parse_args()
+    if os.environ.get("RS_SOLO_PROFILE") != "1":
+        raise SystemExit("set RS_SOLO_PROFILE=1 (the kernels would wait for peers ncu never runs)")
+    os.environ.setdefault("RS_BARRIER_TIMEOUT_S", "2")
+    import torch
+    from paper_2110_10548_b200 import executor, planner
+    n = args.gpus
+    desc = {2: "b200_flat2", 4: "b200_flat4", 8: "b200_flat8"}[n]
+    prog = planner.synthesize(planner.config_path(desc), [n], [0]).placements[0].programs[args.program]
+    es = 2 if args.dtype == "bf16" else 4
+    elems = (args.mib << 20) // es
+    ctx = executor.Context.local(n, list(range(n)), args.mib << 20)
+    ctx.set_option("ll_max_bytes", 0)  # one-shot receives wait for peer packets: not profilable alone
+    plan = ctx.compile(prog, elems, args.dtype)
+    print("program:", prog.text, "| per-step link bytes per GPU per direction:",
+          [plan.step_bytes(s)[0] for s in range(len(prog.steps))], flush=True)
+    for _ in range(2):
+        plan.run()
+    for o in range(n):
+        torch.cuda.synchronize(o)
+    plan.close()
+    ctx.close()
+
+
+if __name__ == "__main__":
+    main()
