@@ -13,10 +13,15 @@
 //   Reduce         owners = non-roots, slices of R, sum -> root only
 //   AllGather /    owners = the receivers, each pulls a slice of a row from
 //   Broadcast      its holder and fans it out to the other receivers
-// Memory: 16-byte vector loads (ld.global.nc.L1::no_allocate) and stores,
-// 4 vectors in flight per thread per source, coalesced 512 B per warp.
-// Inter-GPU ordering: epoch flags (st.release.sys / ld.acquire.sys) in each
-// rank's heap; no NCCL, no host synchronisation between steps.
+// Small steps run one-shot (LL): every destination sums its own result from
+// flagged 16-byte packets its sources pushed into its LL area (kModeLL).
+// Large AllReduce groups on >= 4 GPUs may use NVLS multimem instead.
+// Memory: 16-byte vector loads (ld.global.nc.L1::no_allocate) and streaming
+// stores, 4 (cross-GPU) or 8 (one GPU) vectors in flight per thread per
+// source, coalesced 512 B per warp.
+// Inter-GPU ordering: epoch flags in each rank's heap (relaxed st.sys behind
+// one fence.acq_rel.sys per CTA; ld.acquire.sys spins); no NCCL, no host
+// synchronisation between steps.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
