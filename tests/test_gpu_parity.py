@@ -303,6 +303,52 @@ def test_config1_full_size_across_gpus():
         ctx.close()
 
 
+@pytest.mark.multigpu
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_interleaved_variants_share_epochs():
+    """Plans of different variants (one-shot single step, one-shot two-step
+    with the relaxed wait, pull, push) share one context's epochs and LL
+    parity regions: run them interleaved many times, in place, and compare
+    with the oracle applied in the same order."""
+    n = min(NGPU, 8)
+    name = {2: "k2_flat", 4: "k4_sock", 8: "k8_sock"}.get(n)
+    if name is None:
+        pytest.skip("GPU count without a golden set")
+    K, progs = golden_programs(name)
+    ctx = executor.Context.local(n, list(range(n)), max_bytes=8 << 20)
+    try:
+        single = progs[0][2]
+        multi = next(p for _, _, p, _ in progs if len(p.steps) >= 2)
+        N_small, N_big = 3001, (1 << 20) + 5
+        plans = [(single, N_small), (multi, N_small), (single, N_big), (multi, N_big)]
+        compiled = []
+        for i, (prog, N) in enumerate(plans):
+            ctx.set_option("push_min_bytes", 0 if i == 3 else -1)
+            compiled.append(ctx.compile(prog, N, "i32"))
+        assert compiled[0].describe()["phase_ll"] == [1]
+        assert all(compiled[1].describe()["phase_ll"])
+        assert not any(compiled[2].describe()["phase_ll"])
+        inputs = numeric.synthetic_inputs(K, N_big, numeric.I32)
+        for d in range(K):
+            ctx.write(d, inputs[d])
+        want = [x.copy() for x in inputs]
+        order = [0, 1, 0, 2, 1, 1, 3, 0, 2, 3, 1, 0, 0, 2, 1, 3] * 3
+        for i in order:
+            compiled[i].run()
+            prog, N = plans[i]
+            head = [x[:N].copy() for x in want]
+            numeric.execute(prog, K, head, numeric.I32)
+            for d in range(K):
+                want[d][:N] = head[d]
+        ctx.synchronize()
+        for d in range(K):
+            assert np.array_equal(ctx.read(d, N_big * 4), want[d].view(np.uint8)), d
+        for p in compiled:
+            p.close()
+    finally:
+        ctx.close()
+
+
 def test_cpp_host_example_end_to_end():
     """C++ host: reference planner API -> redsynth::GpuExecutor::Execute on
     every config-2 (reduce {0,1}) program, int32 identity checked in C++."""
