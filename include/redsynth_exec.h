@@ -96,8 +96,10 @@ int rs_ctx_download(rs_ctx* ctx, int slot, void* host, size_t bytes, void* strea
 /* Number of ranks driven by this process and their CUDA ordinals. */
 int rs_ctx_local_ranks(rs_ctx* ctx, int* count, int* ordinals /* RS_MAX_RANKS */);
 /* Context knobs applied to plans compiled afterwards: "push_min_bytes"
- * (cross-GPU groups moving at least this many bytes use the two-phase
- * store-only variant; -1 disables it; default disabled, env RS_PUSH_MIN_BYTES)
+ * (groups spanning exactly two GPUs moving at least this many bytes use the
+ * push variant: one launch, vector data crosses NVLink as stores only, chunk
+ * flags order landing and reduction; -1 disables it; default 128 MiB, env
+ * RS_PUSH_MIN_BYTES)
  * and "barrier_timeout_ms" (device-side spin limit, default 20 s). Scratch
  * for the push variant is reserved at creation: min(K, 8) buffers per slot on
  * multi-GPU contexts (env RS_SCRATCH_REGIONS). "ll_max_bytes": a step whose

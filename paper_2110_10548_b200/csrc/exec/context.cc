@@ -49,10 +49,7 @@ size_t RoundUp(size_t x, size_t a) { return (x + a - 1) / a * a; }
 absl::Status AllocateRank(Context* ctx, int r) {
   Rank& rank = ctx->ranks[r];
   RS_CUDA(cudaSetDevice(rank.ordinal));
-  int hosted = 0;
-  for (int d = 0; d < ctx->K; ++d) hosted += ctx->slot_rank[d] == r;
-  rank.heap_bytes = kDataOffset + static_cast<size_t>(hosted) * (1 + ctx->scratch_regions) * ctx->slot_stride +
-                    static_cast<size_t>(ctx->world) * 2 * ctx->LLRegionBytes();
+  rank.heap_bytes = ctx->flag_offset[r] + ctx->flag_bytes[r];  // slots, LL area, flags (AssignPositions)
   if (ctx->use_vmm) {
     // cuMemCreate'd heap: shareable as a POSIX fd and bindable to multicast.
     std::vector<int> access{rank.ordinal};
@@ -70,8 +67,8 @@ absl::Status AllocateRank(Context* ctx, int r) {
     rank.heap = static_cast<char*>(heap);
   }
   RS_CUDA(cudaMemset(rank.heap, 0, kDataOffset));
-  if (ctx->ll_capacity > 0) {
-    RS_CUDA(cudaMemset(rank.heap + ctx->ll_offset[r], 0, static_cast<size_t>(ctx->world) * 2 * ctx->LLRegionBytes()));
+  if (ctx->ll_capacity > 0 || ctx->flag_bytes[r] > 0) {
+    RS_CUDA(cudaMemset(rank.heap + ctx->ll_offset[r], 0, rank.heap_bytes - ctx->ll_offset[r]));
   }
   const uint64_t first_epoch = 1;
   RS_CUDA(cudaMemcpy(rank.heap + kEpochOffset, &first_epoch, sizeof(first_epoch), cudaMemcpyHostToDevice));
@@ -110,9 +107,20 @@ void AssignPositions(Context* ctx) {
     if (const char* env = std::getenv("RS_LL_CAPACITY")) ctx->ll_capacity = std::strtoull(env, nullptr, 10) & ~7ull;
     if (const char* env = std::getenv("RS_LL_MAX_BYTES")) ctx->ll_max_bytes = std::strtoull(env, nullptr, 10);
   }
+  if (const char* env = std::getenv("RS_FLAG_CHUNK")) {
+    const uint64_t c = std::strtoull(env, nullptr, 10) & ~15ull;
+    if (c >= (16u << 10)) ctx->flag_chunk = c;
+  }
   ctx->ll_offset.assign(ctx->world, 0);
+  ctx->flag_offset.assign(ctx->world, 0);
+  ctx->flag_bytes.assign(ctx->world, 0);
   for (int r = 0; r < ctx->world; ++r) {
     ctx->ll_offset[r] = kDataOffset + static_cast<size_t>(next[r]) * (1 + ctx->scratch_regions) * ctx->slot_stride;
+    ctx->flag_offset[r] = ctx->ll_offset[r] + static_cast<size_t>(ctx->world) * 2 * ctx->LLRegionBytes();
+    if (ctx->world > 1) {
+      const uint64_t chunks = (ctx->slot_stride + ctx->flag_chunk - 1) / ctx->flag_chunk;
+      ctx->flag_bytes[r] = static_cast<uint64_t>(next[r]) * (1 + ctx->scratch_regions) * chunks * sizeof(uint64_t);
+    }
   }
 }
 

@@ -36,6 +36,13 @@ constexpr uint16_t kModeNvlsAllReduce = 1;
 // destinations receive the sum of the sources in order (tagged sources are
 // waited for by flag). Whole 8-byte packets cover [lo & ~7, round8(hi)).
 constexpr uint16_t kModeLL = 2;
+// Push variant: kModeFlagSend copies src -> dst (owner's memory) one
+// kFlagChunk piece at a time and then sets that chunk's flag (the pointer
+// after dst) to the epoch; kModeFlagRecv sums its sources like kModeSum after
+// waiting, per chunk, for each source's flag (nsrc pointers after the dsts,
+// null = local source, no wait).
+constexpr uint16_t kModeFlagSend = 3;
+constexpr uint16_t kModeFlagRecv = 4;
 
 // Everything one rank's kernel for one step needs (passed by value).
 struct StepArgs {
@@ -67,6 +74,7 @@ struct StepArgs {
   uint32_t num_steps;
   uint64_t timeout_ns;
   uint64_t ll_parity_stride;  // bytes between the two parity regions of an LL block
+  uint32_t flag_chunk;        // push-variant chunk (bytes per flag)
 };
 
 // Vector work is cut into pieces of kPieceBytes; a CTA walks a piece in
@@ -75,6 +83,9 @@ constexpr uint32_t kPieceBytes = 64u << 10;
 // LL pieces: 8 packets (64 payload bytes) per thread of a 512-thread CTA,
 // all in flight at once.
 constexpr uint32_t kLLPieceBytes = 32u << 10;
+// Default push-variant chunk (one flag each); also the piece size of
+// flagged tasks (Context::flag_chunk, StepArgs::flag_chunk).
+constexpr uint32_t kFlagChunk = 256u << 10;  // measured: 64 KiB -3 %, 1 MiB -3 % at K=2
 
 cudaError_t LaunchStep(const StepArgs& args, int grid, int block, int unroll, cudaStream_t stream);
 

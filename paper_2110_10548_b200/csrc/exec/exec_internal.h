@@ -28,6 +28,8 @@ namespace rs {
 //   then           the one-shot (LL) receive area when world > 1: per sender
 //                  rank, two parity regions of 2 * ll_capacity bytes (16-byte
 //                  packets {data0, flag, data1, flag} carry 8 payload bytes)
+//   then           push-variant chunk flags when world > 1: one uint64 per
+//                  64 KiB chunk of every hosted slot buffer and scratch region
 constexpr size_t kInboxOffset = 0;
 constexpr size_t kCounterOffset = 256;
 constexpr size_t kErrorOffset = 512;
@@ -66,6 +68,10 @@ constexpr int kMcRegion = -2;  // Ref{mc group index, kMcRegion}: a multicast ba
 // region, biased so that the packet of payload byte x sits at +2x (the kernel
 // adds the parity). Tagged with bit 0 in the pointer table.
 constexpr int kLLRegion = -3;
+// Ref{flag id, kFlagRegion, ll_recv = rank, ll_off = byte offset}: a flag
+// block of the push variant in that rank's flag area; kNullRegion: nullptr.
+constexpr int kFlagRegion = -4;
+constexpr int kNullRegion = -5;
 constexpr size_t kMaxMcGroups = 32;  // multicast objects per context (switch resources)
 
 struct Ref {
@@ -92,11 +98,13 @@ class Context {
   std::vector<int> slot_position;  // slot -> index among its rank's slots
   std::vector<Rank> ranks;
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
-  // Cross-GPU sum/copy groups whose data is at least this many bytes use the
-  // two-phase push variant (stores only over NVLink); smaller ones the
-  // one-pass pull-sum-push variant. Off by default: measured +1.5-3% at K=2
-  // for >= 256 MiB but -25% at K=4 (profiles/r01_tune_push*.log).
-  uint64_t push_min_bytes = ~0ull;
+  // Sum/copy groups spanning exactly two GPUs whose data is at least this
+  // many bytes use the push variant (one launch, vector bodies cross NVLink
+  // as stores only, chunk flags order landing and reduction); the others
+  // the one-pass pull-sum-push variant. K=2 AllReduce: push 648-697 GB/s
+  // bus vs pull 629-667 from 128 MiB to 1 GiB, slower below 64 MiB
+  // (profiles/r01_sweep_k2_push_vs_pull.txt).
+  uint64_t push_min_bytes = 128ull << 20;
   // NVLS: AllReduce groups of >= nvls_min_group slots on distinct GPUs use
   // multimem.ld_reduce + multimem.st through the NVSwitch (needs a VMM heap,
   // RS_NVLS=1 at creation; sums then follow the switch's order: f32/bf16
@@ -120,6 +128,9 @@ class Context {
   uint64_t ll_capacity = 0;
   uint64_t ll_max_bytes = 0;
   std::vector<size_t> ll_offset;  // per rank: its LL area within its heap
+  std::vector<size_t> flag_offset;  // per rank: push-variant chunk flags (after the LL area)
+  std::vector<uint64_t> flag_bytes;
+  uint64_t flag_chunk = kFlagChunk;  // push-variant chunk (RS_FLAG_CHUNK at creation)
   ExchangeFn exchange = nullptr;  // host all-gather (multi-process NVLS setup)
   void* exchange_user = nullptr;
   std::map<std::vector<int>, std::unique_ptr<McGroup>> mc_groups;
@@ -132,6 +143,8 @@ class Context {
   uint64_t LLRegionBytes() const { return 2 * ll_capacity; }
   char* RefPtr(int viewer, const Ref& r) const {
     if (r.region == kMcRegion) return reinterpret_cast<char*>(mc_index[r.slot]->va[viewer]);
+    if (r.region == kNullRegion) return nullptr;
+    if (r.region == kFlagRegion) return ranks[viewer].view[r.ll_recv] + flag_offset[r.ll_recv] + r.ll_off;
     if (r.region == kLLRegion) {
       const uintptr_t p = reinterpret_cast<uintptr_t>(ranks[viewer].view[r.ll_recv]) + ll_offset[r.ll_recv] +
                           static_cast<uintptr_t>(r.ll_send) * 2 * LLRegionBytes() + static_cast<uintptr_t>(r.ll_off);

@@ -44,6 +44,14 @@ struct ProtoTask {
   std::vector<Ref> src;  // summation order
   std::vector<Ref> dst;
   int mc = -1;  // >= 0: NVLS AllReduce through multicast group mc (vector body)
+  // Push variant (one launch, chunk flags): a landing task (flag_send >= 0)
+  // copies its vector body into the owner's memory chunk by chunk and raises
+  // flag block `flag_send` per chunk; a reducing task waits for src_flag[i]
+  // (-1: no wait) per chunk. Unaligned edges are not pushed: the reducing
+  // task's edges pull from edge_src and store to edge_dst.
+  int flag_send = -1;
+  std::vector<int> src_flag;
+  std::vector<Ref> edge_src, edge_dst;
 };
 
 Ref Buf(int slot) { return Ref{slot, -1}; }
@@ -143,6 +151,7 @@ struct Compiler {
   RowGeometry geo;
   std::vector<uint64_t> vid;  // content id of (slot, row)
   uint64_t next_id;
+  int next_flag = 0;  // flag blocks of the push variant (per plan)
 
   Compiler(Context* c, size_t elems, size_t esize, int dt)
       : ctx(c), K(c->K), dtype(dt), geo(elems, c->K, esize), vid(static_cast<size_t>(c->K) * c->K) {
@@ -156,8 +165,14 @@ struct Compiler {
       if (ctx->slot_rank[d] != ctx->slot_rank[g[0]]) return true;
     return false;
   }
+  // Push only between exactly two GPUs: there it measured +4 % over pull
+  // (668 vs 642 GB/s bus, K=2 256 MiB AllReduce), while with three or more
+  // GPUs pushing into one the switch congests (405-525 vs 622 GB/s at K=4;
+  // profiles/r01_tune_push_flagged.txt).
   bool PushCopies(const std::vector<int>& g, uint64_t bytes) const {
-    return SpansRanks(g) && bytes >= ctx->push_min_bytes && bytes > 0;
+    std::set<int> gpus;
+    for (int d : g) gpus.insert(ctx->slot_rank[d]);
+    return gpus.size() == 2 && bytes >= ctx->push_min_bytes && bytes > 0;
   }
   bool PushSums(const std::vector<int>& g, uint64_t bytes) const {
     return PushCopies(g, bytes) && ctx->scratch_regions >= static_cast<int>(g.size());
@@ -183,14 +198,31 @@ struct Compiler {
         Add(out.b, g[p], parts[j], src, dst_of(j));
         continue;
       }
-      // (A) member i lands its copy of the part in owner p's scratch region i.
-      for (int i = 0; i < n; ++i) {
-        if (i == p) continue;
-        Add(out.a, g[i], parts[j], {Buf(g[i])}, {Ref{g[p], i}});
+      // (A) every member on another GPU lands its copy of the part in owner
+      //     p's scratch region i (members on p's GPU are read in place);
+      // (B) owner p waits for each chunk's flags, sums in group order from
+      //     local memory and stores.
+      const int rp = ctx->slot_rank[g[p]];
+      std::vector<Ref> pull_src;
+      for (int m : g) pull_src.push_back(Buf(m));
+      for (const Range& r : parts[j]) {
+        ProtoTask b{g[p], r, {}, dst_of(j)};
+        for (int i = 0; i < n; ++i) {
+          if (i == p || ctx->slot_rank[g[i]] == rp) {
+            b.src.push_back(Buf(g[i]));
+            b.src_flag.push_back(-1);
+            continue;
+          }
+          ProtoTask a{g[i], r, {Buf(g[i])}, {Ref{g[p], i}}};
+          a.flag_send = next_flag++;
+          b.src.push_back(Ref{g[p], i});
+          b.src_flag.push_back(a.flag_send);
+          out.a.push_back(std::move(a));
+        }
+        b.edge_src = pull_src;
+        b.edge_dst = b.dst;
+        out.b.push_back(std::move(b));
       }
-      // (B) owner p sums in group order from local memory and stores.
-      for (int i = 0; i < n; ++i) src.push_back(i == p ? Buf(g[p]) : Ref{g[p], i});
-      Add(out.b, g[p], parts[j], src, dst_of(j));
     }
   }
 
@@ -221,8 +253,20 @@ struct Compiler {
         for (int m : recv)
           if (m != recv[j]) others.push_back(Buf(m));
         if (push) {
-          Add(out.a, h, parts[j], {Buf(h)}, {Buf(recv[j])});
-          if (!others.empty()) Add(out.b, recv[j], parts[j], {Buf(recv[j])}, others);
+          // (A) the holder lands the part in receiver j's buffer chunk by
+          // chunk; (B) receiver j fans each landed chunk out to the others.
+          std::vector<Ref> all_dst;
+          for (int m : recv) all_dst.push_back(Buf(m));
+          for (const Range& r : parts[j]) {
+            ProtoTask a{h, r, {Buf(h)}, {Buf(recv[j])}};
+            a.flag_send = next_flag++;
+            ProtoTask b{recv[j], r, {Buf(recv[j])}, others};
+            b.src_flag = {a.flag_send};
+            b.edge_src = {Buf(h)};
+            b.edge_dst = all_dst;
+            out.a.push_back(std::move(a));
+            out.b.push_back(std::move(b));
+          }
         } else {
           std::vector<Ref> dst;
           for (int m : recv) dst.push_back(Buf(m));
@@ -424,8 +468,113 @@ void AddTraffic(std::vector<RankStep>& per_rank, const Context& ctx, const Proto
   }
 }
 
+Ref FlagRef(int id) { return Ref{id, kFlagRegion}; }  // rank/offset patched per phase
+Ref NullRef() { return Ref{-1, kNullRegion}; }
+
+// Push-variant tasks: a landing task is its vector body only; a reducing
+// task is its vector body (chunk flags appended to the pointer table) plus
+// edges that pull like the default variant.
+void LayFlagged(RankStep& rs, const ProtoTask& t, uint64_t chunk) {
+  const uint64_t a = (t.range.lo + 15) & ~uint64_t{15};
+  const uint64_t b = t.range.hi & ~uint64_t{15};
+  auto scalar = [&](uint64_t lo, uint64_t hi) {
+    if (hi <= lo || t.edge_dst.empty()) return;
+    Task task{};
+    task.lo = lo;
+    task.hi = hi;
+    task.piece_begin = rs.npieces;
+    task.ptr_begin = static_cast<uint32_t>(rs.ptr_refs.size());
+    task.nsrc = static_cast<uint16_t>(t.edge_src.size());
+    task.ndst = static_cast<uint16_t>(t.edge_dst.size());
+    rs.ptr_refs.insert(rs.ptr_refs.end(), t.edge_src.begin(), t.edge_src.end());
+    rs.ptr_refs.insert(rs.ptr_refs.end(), t.edge_dst.begin(), t.edge_dst.end());
+    rs.npieces += 1;
+    rs.tasks.push_back(task);
+  };
+  const bool body = a < b;
+  if (t.flag_send >= 0) {
+    if (!body) return;
+    Task task{};
+    task.lo = a;
+    task.hi = b;
+    task.piece_begin = rs.npieces;
+    task.ptr_begin = static_cast<uint32_t>(rs.ptr_refs.size());
+    task.nsrc = 1;
+    task.ndst = 1;
+    task.vec = 1;
+    task.mode = kModeFlagSend;
+    rs.ptr_refs.push_back(t.src[0]);
+    rs.ptr_refs.push_back(t.dst[0]);
+    rs.ptr_refs.push_back(FlagRef(t.flag_send));
+    rs.npieces += static_cast<uint32_t>((b - a + chunk - 1) / chunk);
+    rs.tasks.push_back(task);
+    return;
+  }
+  if (!body) {  // < 32 bytes: everything pulls
+    const uint64_t mid = std::min(std::max(a, t.range.lo), t.range.hi);
+    scalar(t.range.lo, mid);
+    scalar(mid, t.range.hi);
+    return;
+  }
+  scalar(t.range.lo, a);
+  if (!t.dst.empty()) {
+    Task task{};
+    task.lo = a;
+    task.hi = b;
+    task.piece_begin = rs.npieces;
+    task.ptr_begin = static_cast<uint32_t>(rs.ptr_refs.size());
+    task.nsrc = static_cast<uint16_t>(t.src.size());
+    task.ndst = static_cast<uint16_t>(t.dst.size());
+    task.vec = 1;
+    task.mode = kModeFlagRecv;
+    rs.ptr_refs.insert(rs.ptr_refs.end(), t.src.begin(), t.src.end());
+    rs.ptr_refs.insert(rs.ptr_refs.end(), t.dst.begin(), t.dst.end());
+    for (int f : t.src_flag) rs.ptr_refs.push_back(f >= 0 ? FlagRef(f) : NullRef());
+    rs.npieces += static_cast<uint32_t>((b - a + chunk - 1) / chunk);
+    rs.tasks.push_back(task);
+  }
+  scalar(b, t.range.hi);
+}
+
+// Places every flag block of a push phase in its owner rank's flag area
+// (one uint64 per chunk) and patches the flag references. Returns false if
+// a rank's area would overflow.
+bool PlaceFlags(const Context& ctx, std::vector<RankStep>& phase) {
+  std::map<int, std::pair<int, uint64_t>> where;  // flag id -> (rank, byte offset)
+  std::vector<uint64_t> cursor(ctx.world, 0);
+  for (int r = 0; r < ctx.world; ++r) {
+    for (const Task& t : phase[r].tasks) {
+      if (t.mode != kModeFlagSend) continue;
+      const Ref& dst = phase[r].ptr_refs[t.ptr_begin + 1];
+      const int id = phase[r].ptr_refs[t.ptr_begin + 2].slot;
+      const int owner_rank = ctx.slot_rank[dst.slot];
+      const uint64_t chunks = (t.hi - t.lo + ctx.flag_chunk - 1) / ctx.flag_chunk;
+      where[id] = {owner_rank, cursor[owner_rank]};
+      cursor[owner_rank] += chunks * sizeof(uint64_t);
+    }
+  }
+  if (!ctx.is_virtual) {
+    for (int r = 0; r < ctx.world; ++r)
+      if (cursor[r] > ctx.flag_bytes[r]) return false;
+  }
+  for (RankStep& rs : phase) {
+    for (Ref& ref : rs.ptr_refs) {
+      if (ref.region != kFlagRegion) continue;
+      auto it = where.find(ref.slot);
+      if (it == where.end()) return false;
+      ref.ll_recv = it->second.first;
+      ref.ll_off = static_cast<int64_t>(it->second.second);
+    }
+  }
+  return true;
+}
+
 // Appends `t` to its owner rank's phase: vector body + scalar head/tail.
-void Lay(RankStep& rs, const ProtoTask& t, uint32_t piece_bytes) {
+void Lay(RankStep& rs, const ProtoTask& t, uint32_t piece_bytes, uint64_t flag_chunk = 0) {
+  if (t.flag_send >= 0 || !t.src_flag.empty()) {
+    LayFlagged(rs, t, flag_chunk);
+    return;
+  }
   auto push = [&](uint64_t lo, uint64_t hi, bool vec) {
     if (hi <= lo) return;
     Task task{};
@@ -744,25 +893,29 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
       absl::Status gs = comp.Group(tasks, pre[s], step.groups[gi], step.op);
       if (!gs.ok()) return gs;
     }
-    for (const std::vector<ProtoTask>* list : {&tasks.a, &tasks.b}) {
-      if (list == &tasks.a && list->empty()) continue;
-      plan->phases.emplace_back(R);
-      plan->phase_step.push_back(s);
-      plan->phase_ll.push_back(0);
-      // Piece size per rank: enough pieces to occupy ~2 CTAs per SM (memory
-      // parallelism for remote loads), between 4 KiB and kPieceBytes.
-      std::vector<uint64_t> rank_bytes(R, 0);
-      for (const ProtoTask& t : *list) rank_bytes[ctx->slot_rank[t.owner]] += t.range.hi - t.range.lo;
-      for (int r = 0; r < R; ++r) {
-        uint32_t pb = 4u << 10;
-        while (pb < kPieceBytes && rank_bytes[r] / pb > 2 * 148) pb <<= 1;
-        plan->phases.back()[r].piece_bytes = pb;
-      }
-      for (const ProtoTask& t : *list) {
-        AddTraffic(plan->phases.back(), *ctx, t);
-        RankStep& rs = plan->phases.back()[ctx->slot_rank[t.owner]];
-        Lay(rs, t, rs.piece_bytes);
-      }
+    // One launch: push landing tasks first (every CTA sends before it waits
+    // for chunks), then the reducing / pull tasks.
+    std::vector<ProtoTask> list = std::move(tasks.a);
+    list.insert(list.end(), tasks.b.begin(), tasks.b.end());
+    plan->phases.emplace_back(R);
+    plan->phase_step.push_back(s);
+    plan->phase_ll.push_back(0);
+    // Piece size per rank: enough pieces to occupy ~2 CTAs per SM (memory
+    // parallelism for remote loads), between 4 KiB and kPieceBytes.
+    std::vector<uint64_t> rank_bytes(R, 0);
+    for (const ProtoTask& t : list) rank_bytes[ctx->slot_rank[t.owner]] += t.range.hi - t.range.lo;
+    for (int r = 0; r < R; ++r) {
+      uint32_t pb = 4u << 10;
+      while (pb < kPieceBytes && rank_bytes[r] / pb > 2 * 148) pb <<= 1;
+      plan->phases.back()[r].piece_bytes = pb;
+    }
+    for (const ProtoTask& t : list) {
+      AddTraffic(plan->phases.back(), *ctx, t);
+      RankStep& rs = plan->phases.back()[ctx->slot_rank[t.owner]];
+      Lay(rs, t, rs.piece_bytes, ctx->flag_chunk);
+    }
+    if (comp.next_flag > 0 && !PlaceFlags(*ctx, plan->phases.back())) {
+      return absl::InternalError("push variant: flag area overflow");
     }
   }
 
@@ -771,8 +924,8 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
     for (int r = 0; r < R; ++r) {
       std::set<int> peers;
       for (const Ref& ref : phase[r].ptr_refs) {
-        if (ref.region == kMcRegion) continue;
-        const int q = ref.region == kLLRegion ? ref.ll_recv : ctx->slot_rank[ref.slot];
+        if (ref.region == kMcRegion || ref.region == kNullRegion) continue;
+        const int q = (ref.region == kLLRegion || ref.region == kFlagRegion) ? ref.ll_recv : ctx->slot_rank[ref.slot];
         if (q != r) peers.insert(q);
       }
       phase[r].remote_peers = static_cast<int>(peers.size());
@@ -900,6 +1053,7 @@ void BuildLaunches(Plan* plan) {
       a.inbox = reinterpret_cast<const uint64_t*>(rank.heap + kInboxOffset);
       a.timeout_ns = ctx->timeout_ns;
       a.ll_parity_stride = ctx->LLRegionBytes();
+      a.flag_chunk = static_cast<uint32_t>(ctx->flag_chunk);
       if (ctx->world > 1) {
         for (int q = 0; q < ctx->world; ++q) {
           if (q == r) continue;

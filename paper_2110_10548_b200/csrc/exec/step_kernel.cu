@@ -38,6 +38,16 @@ __device__ __forceinline__ uint4 LoadStream(const void* p) {
   return v;
 }
 
+// L2-coherent load (skips L1): data a peer GPU pushed during this kernel,
+// read after an acquire of its chunk flag.
+__device__ __forceinline__ uint4 LoadCoherent(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ void Store(void* p, const uint4& v) {
 #ifndef RS_STORE_QUAL
 // Streaming stores: measured +2% HBM efficiency in local mode over plain
@@ -160,7 +170,7 @@ template <> struct AccOf<RS_I32> { using T = I32Acc; };
 
 // One block-wide chunk: bytes [begin, end) of the task, 16-byte aligned;
 // thread t handles vectors begin + (u * blockDim + t) * 16, u < kUnroll.
-template <int DT, int kUnroll>
+template <int DT, int kUnroll, bool kCoherent = false>
 __device__ __forceinline__ void VectorChunk(const Task& t, void* const* ptrs, uint64_t begin,
                                             uint64_t end) {
   using Acc = typename AccOf<DT>::T;
@@ -177,7 +187,7 @@ __device__ __forceinline__ void VectorChunk(const Task& t, void* const* ptrs, ui
   const char* s0 = static_cast<const char*>(src[0]);
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u)
-    if (ok[u]) raw[u] = LoadStream(s0 + off[u]);
+    if (ok[u]) raw[u] = kCoherent ? LoadCoherent(s0 + off[u]) : LoadStream(s0 + off[u]);
   if (t.nsrc > 1) {
     Acc acc[kUnroll];
 #pragma unroll
@@ -186,7 +196,7 @@ __device__ __forceinline__ void VectorChunk(const Task& t, void* const* ptrs, ui
       const char* si = static_cast<const char*>(src[i]);
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u)
-        if (ok[u]) raw[u] = LoadStream(si + off[u]);
+        if (ok[u]) raw[u] = kCoherent ? LoadCoherent(si + off[u]) : LoadStream(si + off[u]);
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) acc[u].Add(raw[u]);
     }
@@ -499,6 +509,31 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
       uint64_t begin, end;
       ll_range(t, p, begin, end);
       LLReceive<DT>(t, a.ptrs, begin, end, static_cast<uint32_t>(epoch), parity_off, a.timeout_ns, a.error_flag);
+      continue;
+    }
+    if (t.mode == kModeFlagSend || t.mode == kModeFlagRecv) {
+      // Push variant, one flag_chunk piece: land it and raise its flag, or
+      // wait for every pushed source's flag and reduce it.
+      const uint32_t k = p - t.piece_begin;
+      const uint64_t begin = t.lo + static_cast<uint64_t>(k) * a.flag_chunk;
+      const uint64_t end = min(t.hi, begin + a.flag_chunk);
+      const uint64_t chunk = static_cast<uint64_t>(blockDim.x) * kUnroll * 16u;
+      void* const* flags = a.ptrs + t.ptr_begin + t.nsrc + t.ndst;
+      if (t.mode == kModeFlagRecv) {
+        if (threadIdx.x < t.nsrc && flags[threadIdx.x]) {
+          WaitAtLeast(static_cast<const uint64_t*>(flags[threadIdx.x]) + k, epoch, a.timeout_ns, a.error_flag);
+        }
+        __syncthreads();
+        for (uint64_t c = begin; c < end; c += chunk)
+          VectorChunk<DT, kUnroll, true>(t, a.ptrs, c, min(end, c + chunk));
+      } else {
+        for (uint64_t c = begin; c < end; c += chunk) VectorChunk<DT, kUnroll>(t, a.ptrs, c, min(end, c + chunk));
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          FenceSys();
+          StoreRelaxedSys(static_cast<uint64_t*>(flags[0]) + k, epoch);
+        }
+      }
       continue;
     }
     if (t.vec) {

@@ -61,10 +61,19 @@ def simulate_plan(desc, bufs, dtype):
         return scratch[key]
 
     for step in desc["steps"]:
-        tasks = [t for r in step["ranks"] for t in r["tasks"]]
         for rank, r in enumerate(step["ranks"]):
             for t in r["tasks"]:
                 t["rank"] = rank
+        every = [t for r in step["ranks"] for t in r["tasks"]]
+        # Push variant: landing tasks (mode 3) complete a chunk before the
+        # reducing tasks (mode 4) read it (chunk flags), so they form a
+        # sub-phase of their own; everything else runs after them.
+        for tasks in ([t for t in every if t.get("mode") == 3], [t for t in every if t.get("mode") != 3]):
+            _simulate_tasks(tasks, every, bufs, mem, scratch, es, view, dtype)
+
+
+def _simulate_tasks(tasks, every, bufs, mem, scratch, es, view, dtype):
+    if True:
         for t in tasks:
             t.setdefault("src_region", [-1] * len(t["src"]))
             t.setdefault("dst_region", [-1] * len(t["dst"]))
@@ -76,7 +85,7 @@ def simulate_plan(desc, bufs, dtype):
                     continue
                 assert any(u["mode"] == 2 and (s, -1) in zip(u["src"], u["src_region"]) and
                            (u["lo"], u["hi"]) == (t["lo"], t["hi"]) and t["rank"] in u["sends"]
-                           for u in tasks), f"no sender for LL source {s} of {t}"
+                           for u in every), f"no sender for LL source {s} of {t}"
         # hazard check: per memory object, written intervals vs every other task's accesses
         acc = {}
         for i, t in enumerate(tasks):
@@ -109,7 +118,7 @@ def simulate_plan(desc, bufs, dtype):
             if t.get("mode") == 2:
                 if not t["dst"]:
                     continue
-            elif t["vec"]:
+            elif t["vec"]:  # (push landing / reducing bodies are 16-byte aligned too)
                 assert t["lo"] % 16 == 0 and t["hi"] % 16 == 0
             else:
                 assert t["hi"] - t["lo"] < 16
