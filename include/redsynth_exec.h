@@ -96,9 +96,9 @@ int rs_ctx_download(rs_ctx* ctx, int slot, void* host, size_t bytes, void* strea
 /* Number of ranks driven by this process and their CUDA ordinals. */
 int rs_ctx_local_ranks(rs_ctx* ctx, int* count, int* ordinals /* RS_MAX_RANKS */);
 /* Context knobs applied to plans compiled afterwards: "push_min_bytes"
- * (groups spanning exactly two GPUs moving at least this many bytes use the
- * push variant: one launch, vector data crosses NVLink as stores only, chunk
- * flags order landing and reduction; -1 disables it; default 128 MiB, env
+ * (cross-GPU groups moving at least this many bytes use the push variant:
+ * one launch, vector data crosses NVLink as stores only, chunk flags order
+ * landing and reduction; -1 disables it; default 32 MiB, env
  * RS_PUSH_MIN_BYTES)
  * and "barrier_timeout_ms" (device-side spin limit, default 20 s). Scratch
  * for the push variant is reserved at creation: min(K, 8) buffers per slot on
@@ -117,8 +117,9 @@ int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value);
  * run as multimem.ld_reduce + multimem.st through the NVSwitch. The switch
  * sums in its own order, so f32/bf16 results match the ordered oracle within
  * tolerance instead of bit for bit (i32 never uses NVLS). Options "nvls"
- * (0/1), "nvls_min_group" and "nvls_min_bytes" (default 256 MiB for groups
- * of < 8 GPUs, 16 MiB for >= 8; env RS_NVLS_MIN_BYTES) tune later compiles. */
+ * (0/1), "nvls_min_group" and "nvls_min_bytes" (default: never for groups
+ * of < 8 GPUs, where the push variant is as fast; 16 MiB for >= 8; env
+ * RS_NVLS_MIN_BYTES) tune later compiles. */
 int rs_ctx_nvls(rs_ctx* ctx, int* enabled);
 /* Host all-gather used to set up multicast objects collectively in the
  * one-process-per-GPU mode: fn(send, bytes, recv[world * bytes], user) must

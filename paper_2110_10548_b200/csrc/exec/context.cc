@@ -148,6 +148,7 @@ void ReadTimeoutEnv(Context* ctx) {
   if (const char* env = std::getenv("RS_PUSH_MIN_BYTES")) {
     ctx->push_min_bytes = std::strtoull(env, nullptr, 10);
   }
+  if (const char* env = std::getenv("RS_PUSH_MAX_GPUS")) ctx->push_max_gpus = std::atoi(env);
 }
 
 }  // namespace

@@ -98,13 +98,14 @@ class Context {
   std::vector<int> slot_position;  // slot -> index among its rank's slots
   std::vector<Rank> ranks;
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
-  // Sum/copy groups spanning exactly two GPUs whose data is at least this
-  // many bytes use the push variant (one launch, vector bodies cross NVLink
-  // as stores only, chunk flags order landing and reduction); the others
-  // the one-pass pull-sum-push variant. K=2 AllReduce: push 648-697 GB/s
-  // bus vs pull 629-667 from 128 MiB to 1 GiB, slower below 64 MiB
-  // (profiles/r01_sweep_k2_push_vs_pull.txt).
-  uint64_t push_min_bytes = 128ull << 20;
+  // Cross-GPU sum/copy groups whose data is at least this many bytes use
+  // the push variant (one launch, vector bodies cross NVLink as stores only,
+  // chunk flags order landing and reduction, senders rotate their targets);
+  // smaller ones the one-pass pull-sum-push variant. Measured crossover
+  // ~32 MiB at K=2 and K=4; at K=4 push reaches 661-685 GB/s bus from 128 MiB
+  // to 1 GiB vs pull 596-646 and NVLS 588-681 (profiles/r01_sweep_k4_push.txt).
+  uint64_t push_min_bytes = 32ull << 20;
+  int push_max_gpus = RS_MAX_RANKS;  // RS_PUSH_MAX_GPUS
   // NVLS: AllReduce groups of >= nvls_min_group slots on distinct GPUs use
   // multimem.ld_reduce + multimem.st through the NVSwitch (needs a VMM heap,
   // RS_NVLS=1 at creation; sums then follow the switch's order: f32/bf16
@@ -112,12 +113,12 @@ class Context {
   bool use_vmm = false;
   bool nvls = false;
   int nvls_min_group = 4;
-  // Below this many bytes per group the P2P kernel wins: at n = 4 P2P is
-  // faster up to 128 MiB and NVLS from 256 MiB (1 CTA per SM for multi-peer
-  // pulls; profiles/r01_sweep_n4_nvls_vs_p2p.txt). Groups of >= 8 GPUs move
-  // 1.75 c per GPU with P2P vs 1.125 c with NVLS (1.5 vs 1.25 at n = 4), so
-  // they switch earlier (nvls_min_bytes_n8; not measured: no 8-GPU box).
-  uint64_t nvls_min_bytes = 256ull << 20;
+  // NVLS vs the P2P variants: at n = 4 the push variant is as fast or
+  // faster at every size (685 vs 681 GB/s bus at 1 GiB) and bit-exact, so
+  // groups of < 8 GPUs never use NVLS by default. Groups of >= 8 GPUs move
+  // 1.75 c per GPU with P2P vs 1.125 c with NVLS, so they switch at 16 MiB
+  // (not measured: no 8-GPU box this round).
+  uint64_t nvls_min_bytes = ~0ull;
   uint64_t nvls_min_bytes_n8 = 16ull << 20;
   // One-shot (LL) steps: when every cross-GPU group of a step has its members
   // on distinct GPUs and each GPU sends any peer at most ll_max_bytes, the

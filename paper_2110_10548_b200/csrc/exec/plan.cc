@@ -165,14 +165,14 @@ struct Compiler {
       if (ctx->slot_rank[d] != ctx->slot_rank[g[0]]) return true;
     return false;
   }
-  // Push only between exactly two GPUs: there it measured +4 % over pull
-  // (668 vs 642 GB/s bus, K=2 256 MiB AllReduce), while with three or more
-  // GPUs pushing into one the switch congests (405-525 vs 622 GB/s at K=4;
-  // profiles/r01_tune_push_flagged.txt).
+  // Push needs every sender to land its share in the owner's memory; with
+  // senders walking their targets in rotated order (below) it beats pull
+  // from ~32 MiB at K=2 and K=4 (profiles/r01_sweep_k4_push.txt).
   bool PushCopies(const std::vector<int>& g, uint64_t bytes) const {
     std::set<int> gpus;
     for (int d : g) gpus.insert(ctx->slot_rank[d]);
-    return gpus.size() == 2 && bytes >= ctx->push_min_bytes && bytes > 0;
+    return gpus.size() >= 2 && static_cast<int>(gpus.size()) <= ctx->push_max_gpus && bytes >= ctx->push_min_bytes &&
+           bytes > 0;
   }
   bool PushSums(const std::vector<int>& g, uint64_t bytes) const {
     return PushCopies(g, bytes) && ctx->scratch_regions >= static_cast<int>(g.size());
@@ -896,6 +896,15 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
     // One launch: push landing tasks first (every CTA sends before it waits
     // for chunks), then the reducing / pull tasks.
     std::vector<ProtoTask> list = std::move(tasks.a);
+    // Each sender walks the receiving GPUs starting after itself, so at any
+    // moment the GPUs push into different peers rather than all into one.
+    std::stable_sort(list.begin(), list.end(), [&](const ProtoTask& x, const ProtoTask& y) {
+      auto rot = [&](const ProtoTask& t) {
+        const int from = ctx->slot_rank[t.owner];
+        return (ctx->slot_rank[t.dst[0].slot] - from + R) % R;
+      };
+      return rot(x) < rot(y);
+    });
     list.insert(list.end(), tasks.b.begin(), tasks.b.end());
     plan->phases.emplace_back(R);
     plan->phase_step.push_back(s);

@@ -93,12 +93,15 @@ def test_push_variant_every_program_bit_exact(name, mapping):
                         assert all(desc["slot_rank"][s] == r for s in t["src"]), (prog.text, t)
 
 
-def test_push_only_between_two_gpus():
-    """Three or more GPUs pushing into one congest the switch (measured), so
-    groups spanning more than two GPUs keep the pull variant."""
+def test_push_senders_rotate_targets():
+    """With several GPUs pushing, each sender walks the receiving GPUs
+    starting after itself (GPU r lands in r+1, r+2, ...), so the GPUs push
+    into different peers at any moment instead of all into one (incast)."""
     K, progs = golden_programs("k4_flat")
     _, _, desc = _compile(progs[0][2], K, "one_per_gpu", 1 << 20, numeric.F32, push=True)
-    assert {t["mode"] for rk in desc["steps"][0]["ranks"] for t in rk["tasks"]} == {0}
+    for r, rk in enumerate(desc["steps"][0]["ranks"]):
+        targets = [t["dst"][0] for t in rk["tasks"] if t["mode"] == 3]
+        assert targets == [(r + k) % K for k in range(1, K)], (r, targets)
 
 
 @pytest.mark.parametrize("mapping", ["two_gpus", "four_gpus", "interleaved2"])
