@@ -371,12 +371,11 @@ def main():
         try:  # committed ncu capture of the cross-GPU kernel (tools/profile_p2p.py, profiles/)
             with open(os.path.join(ROOT, "profiles", "r01_ncu_nvlink.json")) as f:
                 caps = json.load(f)
-            cap = caps.get(f"k{min(world, 4)}_p2p") or next(iter(caps.values()))
+            cap = caps.get(f"k{min(world, 4)}_push") or next(iter(caps.values()))  # large steps push
             traffic = cap["nvlrx_user"] + cap["nvltx_user"]
             tnote = (f"traffic = NVLink user bytes rx+tx of one profiled launch ({cap['what']}, replayed alone), "
-                     f"{traffic / (2 * cap['own_share_algorithmic']):.4f} x its algorithmic bytes; link protocol "
-                     f"overhead on top: rx +{cap['nvlrx_total'] / cap['nvlrx_user'] - 1:.0%}, "
-                     f"tx +{cap['nvltx_total'] / cap['nvltx_user'] - 1:.0%} (profiles/r01_ncu_nvlink.txt)")
+                     f"{traffic / cap['own_share_algorithmic']:.4f} x its algorithmic bytes; link headers and flags "
+                     f"on top: tx +{cap['nvltx_total'] / cap['nvltx_user'] - 1:.0%} (profiles/r01_ncu_nvlink.txt)")
         except Exception:
             pass
         roofline = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS, "unit": "GB/s",

@@ -1080,6 +1080,7 @@ void BuildLaunches(Plan* plan) {
         // (results are garbage; never set in production).
         a.nwait = 0;
         a.nfinal = 0;
+        a.solo = 1;
       }
       a.signal_done = rsx.signal_done ? 1u : 0u;
       a.wait_lag = static_cast<uint32_t>(plan->phase_lag[ph]);

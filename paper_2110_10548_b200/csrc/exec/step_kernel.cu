@@ -520,7 +520,7 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
       const uint64_t chunk = static_cast<uint64_t>(blockDim.x) * kUnroll * 16u;
       void* const* flags = a.ptrs + t.ptr_begin + t.nsrc + t.ndst;
       if (t.mode == kModeFlagRecv) {
-        if (threadIdx.x < t.nsrc && flags[threadIdx.x]) {
+        if (threadIdx.x < t.nsrc && flags[threadIdx.x] && !a.solo) {
           WaitAtLeast(static_cast<const uint64_t*>(flags[threadIdx.x]) + k, epoch, a.timeout_ns, a.error_flag);
         }
         __syncthreads();

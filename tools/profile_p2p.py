@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--mib", type=int, default=256)
     ap.add_argument("--program", type=int, default=0)
     ap.add_argument("--dtype", default="bf16")
+    ap.add_argument("--push", type=int, default=0, help="1: push variant (store-only), 0: pull")
     args = ap.parse_args()
     if os.environ.get("RS_SOLO_PROFILE") != "1":
         raise SystemExit("set RS_SOLO_PROFILE=1 (the kernels would wait for peers ncu never runs)")
@@ -35,6 +36,7 @@ def main():
     elems = (args.mib << 20) // es
     ctx = executor.Context.local(n, list(range(n)), args.mib << 20)
     ctx.set_option("ll_max_bytes", 0)  # one-shot receives wait for peer packets: not profilable alone
+    ctx.set_option("push_min_bytes", 0 if args.push else -1)
     plan = ctx.compile(prog, elems, args.dtype)
     print("program:", prog.text, "| per-step link bytes per GPU per direction:",
           [plan.step_bytes(s)[0] for s in range(len(prog.steps))], flush=True)
