@@ -626,6 +626,7 @@ bool LayLL(const Context& ctx, const std::vector<LLSpec>& specs, std::vector<Ran
   // Payload streams: (sender rank, receiver rank, source slot, lo, hi) -> offset.
   std::map<std::tuple<int, int, int, uint64_t, uint64_t>, uint64_t> stream;
   std::vector<uint64_t> pair_bytes(static_cast<size_t>(R) * R, 0);
+  std::vector<uint64_t> sent_bytes(R, 0);
   for (const LLSpec& sp : specs) {
     const int p = ctx.slot_rank[sp.owner];
     int locals = 0;
@@ -641,6 +642,11 @@ bool LayLL(const Context& ctx, const std::vector<LLSpec>& specs, std::vector<Ran
       stream[key] = used;
       used += hi8(sp.range) - lo8(sp.range);
       if (used > budget) return false;
+      // Packets double the bytes and go to every receiver separately: cap a
+      // sender's total at what a K=4 one-shot AllReduce at the budget sends
+      // (3 peers), so wide groups (K=8) switch to pull earlier.
+      sent_bytes[q] += hi8(sp.range) - lo8(sp.range);
+      if (sent_bytes[q] > 3 * budget) return false;
     }
     if (locals > 1) return false;
   }

@@ -316,9 +316,10 @@ def test_ll_ragged_sizes(N):
 
 
 def test_ll_budget_selects_variant():
-    """An AllReduce of D bytes over 8 GPUs sends D to each peer: one-shot at
-    D <= ll_max_bytes, pull above it."""
-    K, progs = golden_programs("k8_flat")
+    """An AllReduce of D bytes over n GPUs sends D to each peer: one-shot at
+    D <= ll_max_bytes per peer and (n-1) D <= 3 ll_max_bytes per sender,
+    pull above."""
+    K, progs = golden_programs("k4_flat")
     prog = progs[0][2]
     ctx = executor.Context.virtual(K, list(range(K)), K)
     ctx.set_option("push_min_bytes", -1)
@@ -329,6 +330,12 @@ def test_ll_budget_selects_variant():
     assert ctx.compile(prog, 16, "f32").describe()["phase_ll"] == [0]
     ctx.set_option("ll_max_bytes", 1 << 30)  # capped by the reserved area (512 KiB)
     assert ctx.compile(prog, (1 << 20) // 4, "f32").describe()["phase_ll"] == [0]
+    K, progs = golden_programs("k8_flat")  # 7 peers: the per-sender cap binds first
+    ctx = executor.Context.virtual(K, list(range(K)), K)
+    ctx.set_option("ll_max_bytes", 64 << 10)
+    D = 3 * (64 << 10) // 7 // 8 * 8
+    assert ctx.compile(progs[0][2], D // 4, "f32").describe()["phase_ll"] == [1]
+    assert ctx.compile(progs[0][2], (D + 64) // 4, "f32").describe()["phase_ll"] == [0]
 
 
 def test_ll_allreduce_sends_from_inside_the_owner_task():
