@@ -206,6 +206,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-serial", action="store_true", help="e2e without overlapping copies across steps")
+    ap.add_argument("--no-graph", action="store_true", help="timed steps launch every program eagerly")
     ap.add_argument("--programs-out", default=None, help="write per-program device times (JSON)")
     ap.add_argument("--workload", default="config2", choices=["config2", "kN"],
                     help="config2: BASELINE config 2 (8 slots); kN: K = N slots, one per GPU")
@@ -313,6 +314,22 @@ def main():
             nccl_us[key] = float(t.item())
         del xbuf
 
+    # The timed step replays one CUDA graph of all programs' launches (epochs
+    # are device resident, so replays chain like eager runs); --no-graph
+    # launches them one by one.
+    graph = None
+    if not args.no_graph:
+        barrier()
+        graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(dev)
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(graph, stream=cap):
+                step()
+        barrier()
+        graph.replay()  # one more warm-up step, through the graph
+        barrier()
+
     sampler = ClockSampler(local_rank) if rank == 0 else None
     if sampler:
         sampler.start()
@@ -321,7 +338,10 @@ def main():
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for _ in range(args.steps):
-        step()
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
     t1.record(stream)
     barrier()
     clocks = sampler.stop() if sampler else None
@@ -436,6 +456,22 @@ def main():
             for p in sets[1][1]:  # warm the second set (untimed)
                 p.run()
         host_out = [{d: torch.empty_like(t).pin_memory() for d, t in host_in.items()} for _ in sets]
+        # the programs of each buffer set as one CUDA graph (as in the timed step)
+        set_graphs = []
+        for _, ps in sets:
+            if args.no_graph:
+                set_graphs.append(None)
+                continue
+            barrier()
+            g = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream(dev)
+            cap.wait_stream(stream)
+            with torch.cuda.stream(cap):
+                with torch.cuda.graph(g, stream=cap):
+                    for p in ps:
+                        p.run()
+            barrier()
+            set_graphs.append(g)
         h2d = torch.cuda.Stream(dev)
         d2h = torch.cuda.Stream(dev)
         h2d_h, d2h_h = executor._stream_handle(h2d), executor._stream_handle(d2h)
@@ -456,8 +492,11 @@ def main():
             up = torch.cuda.Event()
             up.record(h2d)
             stream.wait_event(up)
-            for p in ps:
-                p.run()
+            if set_graphs[x] is not None:
+                set_graphs[x].replay()
+            else:
+                for p in ps:
+                    p.run()
             done = torch.cuda.Event()
             done.record(stream)
             d2h.wait_event(done)
@@ -484,6 +523,7 @@ def main():
                          + ("serial" if len(sets) == 1 else
                             "pipelined over two buffer sets (copies of neighbouring steps overlap compute)"),
                "ms_per_step": round(e2e_ms, 2), "wall_ms_per_step": round(wall_ms, 2)}
+        del set_graphs
         if len(sets) > 1:
             barrier()
             for p in sets[1][1]:
