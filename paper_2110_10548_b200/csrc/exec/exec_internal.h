@@ -218,6 +218,9 @@ absl::Status RunPlan(Plan* plan, void* const* device_bufs, void* const* host_buf
                      void* const* streams);
 
 std::string DescribePlan(const Plan& plan);
+// Launch records (StepArgs + grid) of every (phase, driven rank); called on
+// the first run after compilation or a launch-shape change.
+void BuildLaunches(Plan* plan);
 
 int MaxResidentCtas(int dtype, int threads, int unroll);  // per SM, from the occupancy API
 
