@@ -118,7 +118,9 @@ void AssignPositions(Context* ctx) {
     ctx->ll_offset[r] = kDataOffset + static_cast<size_t>(next[r]) * (1 + ctx->scratch_regions) * ctx->slot_stride;
     ctx->flag_offset[r] = ctx->ll_offset[r] + static_cast<size_t>(ctx->world) * 2 * ctx->LLRegionBytes();
     if (ctx->world > 1) {
-      const uint64_t chunks = (ctx->slot_stride + ctx->flag_chunk - 1) / ctx->flag_chunk;
+      // per (slot, region): its chunks, doubled plus slack for parts split
+      // into several row ranges (each rounds up to whole chunks)
+      const uint64_t chunks = 2 * ((ctx->slot_stride + ctx->flag_chunk - 1) / ctx->flag_chunk) + 64;
       ctx->flag_bytes[r] = static_cast<uint64_t>(next[r]) * (1 + ctx->scratch_regions) * chunks * sizeof(uint64_t);
     }
   }
