@@ -44,6 +44,10 @@ class CompiledProgram {
   // Device time of one run in microseconds (warmup untimed runs, then iters
   // timed back-to-back runs; slowest GPU). Synchronous.
   absl::StatusOr<double> TimeUs(int warmup = 1, int iters = 5);
+  // B200-calibrated cost of one run in microseconds from the plan's own
+  // traffic (rs_plan_predict_us): per launch, launch_us + link bytes /
+  // link_gbs + HBM bytes / hbm_gbs (maxed over GPUs).
+  absl::StatusOr<double> PredictUs(double launch_us, double link_gbs, double hbm_gbs) const;
 
  private:
   friend class GpuExecutor;

@@ -53,6 +53,13 @@ absl::StatusOr<double> CompiledProgram::TimeUs(int warmup, int iters) {
   return us;
 }
 
+absl::StatusOr<double> CompiledProgram::PredictUs(double launch_us, double link_gbs, double hbm_gbs) const {
+  double us = 0;
+  absl::Status s = FromCode(rs_plan_predict_us(plan_, launch_us, link_gbs, hbm_gbs, &us));
+  if (!s.ok()) return s;
+  return us;
+}
+
 int CompiledProgram::launches_per_run() const {
   int n = 0;
   rs_plan_launch_count(plan_, &n);

@@ -7,8 +7,9 @@
 // synthesized program on B200s through redsynth::GpuExecutor (the C-ABI) on
 // buffers of --bytes per device and adds measured columns to the JSON report:
 // per program "measured_us", "bus_GBps" (nccl-tests AllReduce convention over
-// the reduction group) and "measured_rank", per matrix "measured_best" (SURVEY
-// §8(f) item 4). --gpus maps physical device d to CUDA ordinal gpus[d]
+// the reduction group), "measured_rank" and "calibrated_us" (B200 cost model,
+// rs_plan_predict_us), per matrix "measured_best" and "calibrated_best"
+// (SURVEY §8(f) items 3-4). --gpus maps physical device d to CUDA ordinal gpus[d]
 // (default: every device on GPU 0 = local mode).
 #include <algorithm>
 #include <cstdint>
@@ -95,6 +96,11 @@ int Execute(const redsynth::RunRequest& request, const redsynth::Report& report,
         redsynth::ReductionGroupPartition((*matrices)[mi], request.reduction_axes, *system);
     const double n = static_cast<double>(partition.empty() ? 1 : partition[0].size());
     std::vector<double> us(synthesis->programs.size(), 0.0);
+    std::vector<double> cal(synthesis->programs.size(), 0.0);
+    // Calibrated-model constants: launch latency 3 us when every
+    // slot shares one GPU, 8 us across GPUs; 650 GB/s link, 5,967 GB/s HBM.
+    const bool one_gpu = std::all_of(gpus.begin(), gpus.end(), [&](int o) { return o == gpus[0]; });
+    const double launch_us = one_gpu ? 3.0 : 8.0;
     for (size_t p = 0; p < synthesis->programs.size(); ++p) {
       auto compiled = (*gpu)->Compile(synthesis->programs[p].lowered, elems, type);
       if (!compiled.ok()) {
@@ -107,6 +113,8 @@ int Execute(const redsynth::RunRequest& request, const redsynth::Report& report,
         return 1;
       }
       us[p] = *t;
+      auto c = (*compiled)->PredictUs(launch_us, 650.0, 5967.0);
+      if (c.ok()) cal[p] = *c;
     }
     // Measured rank (stable on ties, like RankPrograms).
     std::vector<size_t> order(us.size());
@@ -120,9 +128,12 @@ int Execute(const redsynth::RunRequest& request, const redsynth::Report& report,
       prog["measured_us"] = us[id];
       prog["bus_GBps"] = static_cast<double>(bytes) / (us[id] * 1e-6) * 2.0 * (n - 1.0) / n / 1e9;
       prog["measured_rank"] = rank_of[id];
+      prog["calibrated_us"] = cal[id];
     }
     if (!order.empty()) {
       section["measured_best"] = {{"program", static_cast<int>(order[0])}, {"us", us[order[0]]}};
+      const size_t cb = static_cast<size_t>(std::min_element(cal.begin(), cal.end()) - cal.begin());
+      section["calibrated_best"] = {{"program", static_cast<int>(cb)}, {"measured_us", us[cb]}};
     }
   }
   doc["executed"] = {{"gpus", gpus}, {"dtype", dtype_name}, {"iters", iters},

@@ -379,5 +379,6 @@ def test_synth_cli_execute_mode(tmp_path):
         assert m["measured_best"]["us"] > 0
         ranks = sorted(p["measured_rank"] for p in m["programs"])
         assert ranks == list(range(1, len(m["programs"]) + 1))
+        assert m["calibrated_best"]["measured_us"] > 0
         for p in m["programs"]:
-            assert p["measured_us"] > 0 and p["bus_GBps"] > 0
+            assert p["measured_us"] > 0 and p["bus_GBps"] > 0 and p["calibrated_us"] > 0
