@@ -139,10 +139,11 @@ struct LLSpec {
   std::vector<int> src;
 };
 
-// Task lists of the two phases of one program step.
+// Tasks of one program step: push landing tasks (a) and everything else
+// (b); both go into the step's single launch, landing tasks first.
 struct StepTasks {
-  std::vector<ProtoTask> a;  // push scatter phase (empty when nothing pushes)
-  std::vector<ProtoTask> b;  // pull tasks and push reduce/fan-out tasks
+  std::vector<ProtoTask> a;  // push landing tasks (empty when nothing pushes)
+  std::vector<ProtoTask> b;  // pull tasks and push reducing / fan-out tasks
 };
 
 struct Compiler {
@@ -842,7 +843,7 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
   }
   if (const char* v = std::getenv("RS_MAX_CTAS")) plan->max_ctas = std::max(0, std::atoi(v));
 
-  // 2./3. Tasks per step, laid out into one or two phases.
+  // 2./3. Tasks per step, laid out into one launch phase per step.
   Compiler comp(ctx, elems, es, dtype);
   const int R = ctx->world;
   std::vector<std::vector<int>> gidx(num_steps, std::vector<int>(K, -1));  // -1 = idle
