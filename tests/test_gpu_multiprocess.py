@@ -119,6 +119,38 @@ def _worker(rank, world, port, result_dir):
                 del g
                 plan.close()
                 dist.barrier()
+        # Push variant across processes: chunk flags live in the owners'
+        # heaps (IPC-mapped); eager chains and a graph replay.
+        ctx.set_option("push_min_bytes", 0)
+        ctx.set_option("ll_max_bytes", 0)
+        N, dt = (1 << 20) - 5, numeric.I32
+        inputs = numeric.synthetic_inputs(K, N, dt)
+        for _, _, prog, _ in progs[:6]:
+            ctx.write(rank, inputs[rank])
+            plan = ctx.compile(prog, N, dt)
+            modes = {t["mode"] for st in plan.describe()["steps"] for rk in st["ranks"] for t in rk["tasks"]}
+            if 3 not in modes:
+                raise AssertionError(f"expected push landing tasks: {prog.text}")
+            torch.cuda.synchronize()
+            dist.barrier()
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                plan.run()
+                plan.run()
+                with torch.cuda.graph(g, stream=s):
+                    plan.run()
+            torch.cuda.synchronize()
+            g.replay()
+            ctx.synchronize()
+            want = [x.copy() for x in inputs]
+            for _ in range(3):  # two eager runs + one replay
+                numeric.execute(prog, K, want, dt)
+            if not np.array_equal(ctx.read(rank, N * 4), want[rank].view(np.uint8)):
+                raise AssertionError(f"push mismatch rank {rank}: {prog.text}")
+            del g
+            plan.close()
+            dist.barrier()
         ctx.close()
         dist.destroy_process_group()
     except Exception:
