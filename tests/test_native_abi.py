@@ -53,3 +53,26 @@ def test_null_arguments_are_invalid():
     assert lib.rs_ctx_create(2, None, 1 << 20, None) == nat.RS_INVALID_ARGUMENT
     assert lib.rs_plan_run(None, None, None) == nat.RS_INVALID_ARGUMENT
     assert lib.rs_ctx_destroy(None) == nat.RS_OK
+
+
+def test_option_and_model_errors_on_a_planning_context():
+    """Options and the cost model on a planning-only (virtual) context: bad
+    keys / values are INVALID_ARGUMENT with a message naming the valid keys;
+    runs are refused (no GPU work is attempted)."""
+    from paper_2110_10548_b200 import executor
+    from paper_2110_10548_b200.planner import LoweredProgram
+    ctx = executor.Context.virtual(4, [0, 1, 2, 3], 4)
+    lib = nat.lib()
+    assert lib.rs_ctx_set_option(ctx._h, b"no_such_option", 1) == nat.RS_INVALID_ARGUMENT
+    assert b"ll_max_bytes" in lib.rs_last_error()
+    for key in (b"push_min_bytes", b"ll_max_bytes", b"nvls_min_bytes", b"barrier_timeout_ms"):
+        assert lib.rs_ctx_set_option(ctx._h, key, 1 << 20) == nat.RS_OK
+    plan = ctx.compile(LoweredProgram(steps=[(0, [[0, 1, 2, 3]])]), 1024, "f32")
+    us = ctypes.c_double()
+    assert lib.rs_plan_predict_us(plan._h, 8.0, -1.0, 6000.0, ctypes.byref(us)) == nat.RS_INVALID_ARGUMENT
+    assert lib.rs_plan_predict_us(plan._h, 8.0, 650.0, 6000.0, None) == nat.RS_INVALID_ARGUMENT
+    assert lib.rs_plan_predict_us(plan._h, 8.0, 650.0, 6000.0, ctypes.byref(us)) == nat.RS_OK and us.value > 8.0
+    assert lib.rs_plan_run(plan._h, None, None) == nat.RS_FAILED_PRECONDITION
+    assert b"virtual" in lib.rs_last_error()
+    plan.close()
+    ctx.close()
