@@ -349,6 +349,27 @@ def test_interleaved_variants_share_epochs():
         ctx.close()
 
 
+@pytest.mark.multigpu
+@pytest.mark.skipif(NGPU < 3, reason="needs >= 3 GPUs")
+def test_three_gpus_shuffled_slots_every_variant():
+    """8 slots shuffled over 3 GPUs (uneven, non power of two): one-shot,
+    pull and push steps, bit-exact."""
+    import random
+    rng = random.Random(3)
+    ords = [d % 3 for d in range(8)]
+    rng.shuffle(ords)
+    ctx = executor.Context.local(8, ords, max_bytes=16 << 20)
+    try:
+        K, progs = golden_programs("cfg2_r01")
+        for _, _, prog, _ in progs[::60]:
+            _run(ctx, prog, K, 3001, numeric.BF16, runs=2)
+        ctx.set_option("push_min_bytes", 0)
+        for _, _, prog, _ in progs[::90]:
+            _run(ctx, prog, K, (4 << 20) - 3, numeric.I32, runs=2)
+    finally:
+        ctx.close()
+
+
 def test_cpp_host_example_end_to_end():
     """C++ host: reference planner API -> redsynth::GpuExecutor::Execute on
     every config-2 (reduce {0,1}) program, int32 identity checked in C++."""

@@ -370,3 +370,30 @@ def test_calibrated_cost_model():
     assert l1 == 0 and abs(plan1.predict_us(3.0, 650.0, 6000.0) - (3.0 + h1 / 6000e3)) < 1e-6
     with pytest.raises(ExecError):
         plan.predict_us(8.0, 0.0, 6000.0)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_slot_to_gpu_mappings(seed):
+    """Arbitrary slot -> GPU maps (3, 5, 6, 7 GPUs, slots shuffled) under
+    every variant threshold setting: hazard-free and bit-exact."""
+    rng = random.Random(100 + seed)
+    world = [3, 5, 6, 7, 2, 4][seed]
+    for name in ("cfg2_r01", "cfg3_r12", "k8_sock"):
+        K, progs = golden_programs(name)
+        slot_rank = [d % world for d in range(K)]
+        rng.shuffle(slot_rank)
+        for _, _, prog, _ in rng.sample(progs, min(12, len(progs))):
+            for push, ll in ((False, False), (True, False), (False, True)):
+                ctx = executor.Context.virtual(K, slot_rank, world)
+                ctx.set_option("push_min_bytes", 0 if push else -1)
+                ctx.set_option("ll_max_bytes", (256 << 10) if ll else 0)
+                N = rng.choice([7, 100, 2049, 5000])
+                dtype = rng.choice([numeric.F32, numeric.BF16, numeric.I32])
+                desc = ctx.compile(prog, N, dtype).describe()
+                inputs = numeric.synthetic_inputs(K, N, dtype)
+                want = [x.copy() for x in inputs]
+                numeric.execute(prog, K, want, dtype, nthreads=1)
+                got = [x.copy() for x in inputs]
+                simulate_plan(desc, got, dtype)
+                for d in range(K):
+                    assert np.array_equal(got[d].view(np.uint8), want[d].view(np.uint8)), (prog.text, slot_rank, d)
