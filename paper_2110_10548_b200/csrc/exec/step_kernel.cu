@@ -375,6 +375,96 @@ __device__ __forceinline__ void LLSend(const Task& t, void* const* ptrs, uint64_
   }
 }
 
+// Up to kLLWide sources: every source's packets of a batch are loaded before
+// any flag is checked, so the sources' latencies overlap (a group of n GPUs
+// otherwise pays n-1 dependent local round trips per batch).
+constexpr int kLLWide = 4;
+
+template <int DT>
+__device__ __forceinline__ void StoreLLResult(const Task& t, void* const* dst, uint64_t x, uint2 out) {
+  constexpr uint32_t kEs = DT == RS_BF16 ? 2 : 4;
+  const bool whole = x >= t.lo && x + 8 <= t.hi;
+  for (int j = 0; j < t.ndst; ++j) {
+    const uintptr_t d = reinterpret_cast<uintptr_t>(dst[j]);
+    if (d & 1u) continue;
+    char* base = reinterpret_cast<char*>(d);
+    if (whole) {
+      *reinterpret_cast<uint2*>(base + x) = out;
+      continue;
+    }
+    // Edge packet: only the elements inside [lo, hi).
+    const char* bytes = reinterpret_cast<const char*>(&out);
+    for (uint32_t e = 0; e < 8; e += kEs) {
+      if (x + e < t.lo || x + e >= t.hi) continue;
+      if (kEs == 2) *reinterpret_cast<uint16_t*>(base + x + e) = *reinterpret_cast<const uint16_t*>(bytes + e);
+      else *reinterpret_cast<uint32_t*>(base + x + e) = *reinterpret_cast<const uint32_t*>(bytes + e);
+    }
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ void LLReceiveWide(const Task& t, void* const* src, void* const* dst, const char* local,
+                                              uint64_t begin, uint64_t end, uint32_t flag, uint64_t parity_off,
+                                              uint64_t timeout_ns, int* error_flag) {
+  constexpr int kB = 4;  // packets per thread per pass
+  const uint64_t stride = static_cast<uint64_t>(blockDim.x) * 8u;
+  const int n = t.nsrc;
+  const char* base[kLLWide];
+#pragma unroll
+  for (int i = 0; i < kLLWide; ++i) {
+    const uintptr_t s = i < n ? reinterpret_cast<uintptr_t>(src[i]) : 0;
+    base[i] = (s & 1u) ? reinterpret_cast<const char*>((s & ~uintptr_t{1}) + parity_off) : nullptr;
+  }
+  for (uint64_t x0 = begin + static_cast<uint64_t>(threadIdx.x) * 8u; x0 < end; x0 += stride * kB) {
+    uint4 pk[kLLWide][kB];
+    uint2 mine[kB];
+#pragma unroll
+    for (int b = 0; b < kB; ++b) {
+      const uint64_t x = x0 + b * stride;
+      mine[b] = (local && x < end) ? *reinterpret_cast<const uint2*>(local + x) : make_uint2(0, 0);
+    }
+#pragma unroll
+    for (int i = 0; i < kLLWide; ++i) {  // every source's loads in flight at once
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+        const uint64_t x = x0 + b * stride;
+        pk[i][b] = (base[i] && x < end) ? LoadVolatile16(base[i] + 2 * x) : make_uint4(0, flag, 0, flag);
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < kB; ++b) {
+      const uint64_t x = x0 + b * stride;
+      if (x >= end) continue;
+      uint2 out = mine[b];
+      float f[4];
+#pragma unroll
+      for (int i = 0; i < kLLWide; ++i) {
+        if (i >= n) break;
+        uint2 v = mine[b];
+        if (base[i]) {
+          if (pk[i][b].y != flag || pk[i][b].w != flag) {
+            const uint2 late = LoadLL(base[i] + 2 * x, flag, timeout_ns, error_flag);
+            pk[i][b] = make_uint4(late.x, flag, late.y, flag);
+          }
+          v = make_uint2(pk[i][b].x, pk[i][b].z);
+        }
+        if constexpr (DT == RS_BF16) {
+          float g[4];
+          BF16Acc::Widen(v.x, g[0], g[1]);
+          BF16Acc::Widen(v.y, g[2], g[3]);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) f[k] = i == 0 ? g[k] : __fadd_rn(f[k], g[k]);
+        }
+        out = i == 0 ? v : AddPacket<DT>(out, v);
+      }
+      if constexpr (DT == RS_BF16) {
+        if (n > 1) out = make_uint2(BF16Acc::Narrow(f[0], f[1]), BF16Acc::Narrow(f[2], f[3]));
+      }
+      StoreLLResult<DT>(t, dst, x, out);
+    }
+  }
+}
+
 // Sweep 2 over the same packets (same thread per packet, so a task that sends
 // its own slot reads every value before overwriting it): wait for the tagged
 // sources, sum all sources in order, store the elements inside [lo, hi).
@@ -391,6 +481,13 @@ __device__ __forceinline__ void LLReceive(const Task& t, void* const* ptrs, uint
   if (!any_result) return;
   const char* local = LLLocal(t, src);
   const uint64_t stride = static_cast<uint64_t>(blockDim.x) * 8u;
+  // Small pieces with >= 2 remote sources: overlap the sources' latencies
+  // (measured K=4 1 KiB AllReduce 9.4 -> 7.9 us); larger pieces keep the
+  // 8-deep per-source batches (the wide path was slower from 16 KiB).
+  if (t.nsrc >= 3 && t.nsrc <= kLLWide && end - begin <= stride * 4) {
+    LLReceiveWide<DT>(t, src, dst, local, begin, end, flag, parity_off, timeout_ns, error_flag);
+    return;
+  }
   for (uint64_t x0 = begin + static_cast<uint64_t>(threadIdx.x) * 8u; x0 < end; x0 += stride * kLLBatch) {
     uint2 mine[kLLBatch], out[kLLBatch];
     float f[kLLBatch][4];
