@@ -399,7 +399,8 @@ def main():
         except Exception:
             pass
         roofline = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
-                    "frac": round(achieved / NVLINK_PEAK_GBS, 4), "traffic": traffic,
+                    "frac": round(achieved / NVLINK_PEAK_GBS, 4), "frac_of_nominal_900": round(achieved / 900.0, 4),
+                    "traffic": traffic,
                     "note": "per-GPU per-direction link bytes of SURVEY §8(d) (T_roof = sum_s max_g f*c_g) "
                             "over the measured step; peak = measured peer copy 770 GB/s (900 nominal); " + tnote}
 
