@@ -102,9 +102,9 @@ int rs_ctx_local_ranks(rs_ctx* ctx, int* count, int* ordinals /* RS_MAX_RANKS */
  * RS_PUSH_MIN_BYTES)
  * and "barrier_timeout_ms" (device-side spin limit, default 20 s). Scratch
  * for the push variant is reserved at creation: min(K, 8) buffers per slot on
- * multi-GPU contexts (env RS_SCRATCH_REGIONS). "ll_max_bytes": a step in
- * which no GPU sends a peer more than this many bytes (nor more than three
- * times it in total) runs one-shot (LL): sources are pushed as flagged
+ * multi-GPU contexts (env RS_SCRATCH_REGIONS). "ll_max_bytes": a step whose
+ * cross-GPU groups have one member per GPU and in which no GPU sends a peer
+ * more than this many bytes runs one-shot (LL): sources are pushed as flagged
  * 16-byte packets into each receiver's LL area and every destination sums
  * locally, in group order (bit-exact like the pull path); 0 disables it
  * (default 256 KiB, env RS_LL_MAX_BYTES, capped by the per-peer area reserved

@@ -7,9 +7,9 @@
 // 2. Turns every group of every step into owner tasks over row ranges; row r
 //    of a slot buffer is elements [floor(rN/K), floor((r+1)N/K)) (SURVEY.md
 //    §8(a) a4). One launch per step, variants per step/group:
-//      one-shot  small steps: sources push flagged 16-byte packets (also to
-//                co-located members), every destination sums its own
-//                result (LayLL);
+//      one-shot  small steps whose cross-GPU groups have one member per GPU:
+//                sources push flagged 16-byte packets, every destination
+//                sums its own result (LayLL);
 //      pull      owners load (peer) sources, sum, store (peer) results;
 //      push      >= push_min_bytes: sources land the owners' parts in their
 //                scratch chunk by chunk behind flags (rotated targets),
@@ -617,9 +617,9 @@ void Lay(RankStep& rs, const ProtoTask& t, uint32_t piece_bytes, uint64_t flag_c
 }
 
 // Lays a one-shot step into `phase` (one RankStep per rank). Returns false
-// (phase untouched) when the step does not fit the LL scheme: a GPU pair
-// exchanging more than the LL budget, a sender over its total cap, or a send
-// whose bytes another task of the step overwrites.
+// (phase untouched) when the step does not fit the LL scheme: a cross-GPU
+// group with two members on one GPU, a GPU pair exchanging more than the LL
+// budget, or a send whose bytes another task of the step overwrites.
 bool LayLL(const Context& ctx, const std::vector<LLSpec>& specs, std::vector<RankStep>& phase) {
   const int R = ctx.world;
   const uint64_t budget = std::min<uint64_t>(ctx.ll_max_bytes, ctx.ll_capacity);
@@ -631,13 +631,13 @@ bool LayLL(const Context& ctx, const std::vector<LLSpec>& specs, std::vector<Ran
   std::vector<uint64_t> sent_bytes(R, 0);
   for (const LLSpec& sp : specs) {
     const int p = ctx.slot_rank[sp.owner];
+    int locals = 0;
     for (int x : sp.src) {
-      // Every source but the owner itself arrives as packets, including
-      // members on the owner's own GPU (its own-rank block): their slots may
-      // be overwritten by their own tasks during the step, the packets are
-      // snapshots taken before that.
-      if (x == sp.owner) continue;
       const int q = ctx.slot_rank[x];
+      if (q == p) {
+        ++locals;
+        continue;
+      }
       auto key = std::make_tuple(q, p, x, sp.range.lo, sp.range.hi);
       if (stream.count(key)) continue;
       uint64_t& used = pair_bytes[static_cast<size_t>(q) * R + p];
@@ -650,6 +650,7 @@ bool LayLL(const Context& ctx, const std::vector<LLSpec>& specs, std::vector<Ran
       sent_bytes[q] += hi8(sp.range) - lo8(sp.range);
       if (sent_bytes[q] > 3 * budget) return false;
     }
+    if (locals > 1) return false;
   }
   auto ll_ref = [&](int slot, int recv, int send, uint64_t off, const Range& rg) {
     Ref r{slot, kLLRegion};
@@ -673,7 +674,7 @@ bool LayLL(const Context& ctx, const std::vector<LLSpec>& specs, std::vector<Ran
     Proto t{p, sp.range, {}, {Buf(sp.owner)}};
     for (int x : sp.src) {
       const int q = ctx.slot_rank[x];
-      t.src.push_back(x == sp.owner ? Buf(x) : ll_ref(x, p, q, stream[{q, p, x, sp.range.lo, sp.range.hi}], sp.range));
+      t.src.push_back(q == p ? Buf(x) : ll_ref(x, p, q, stream[{q, p, x, sp.range.lo, sp.range.hi}], sp.range));
     }
     if (std::find(sp.src.begin(), sp.src.end(), sp.owner) != sp.src.end())
       fused[{sp.owner, sp.range.lo, sp.range.hi}] = recv.size();
