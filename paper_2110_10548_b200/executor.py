@@ -342,6 +342,13 @@ class Plan:
         nat.check(nat.lib().rs_plan_step_bytes(self._h, step, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value
 
+    def time_us(self, warmup: int = 1, iters: int = 5) -> float:
+        """Device time of one run (rs_plan_time: back-to-back runs bracketed by
+        CUDA events on every local GPU's stream, slowest GPU). Synchronous."""
+        us = ctypes.c_double()
+        nat.check(nat.lib().rs_plan_time(self._h, int(warmup), int(iters), ctypes.byref(us)))
+        return us.value
+
     def predict_us(self, launch_us: float = 8.0, link_gbs: float = 650.0, hbm_gbs: float = 6000.0) -> float:
         """B200-calibrated cost of one run from the plan's own traffic
         (rs_plan_predict_us); defaults = measured per-step latency (K=4),
