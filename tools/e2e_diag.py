@@ -1,3 +1,6 @@
+"""Diagnostic: per-slot upload / run / download timings of the end-to-end
+path (rs_ctx_upload, rs_plan_run, rs_ctx_download) on one GPU, to check
+which stream each copy lands on. python tools/e2e_diag.py"""
 import sys, time, torch
 sys.path.insert(0, '.')
 from paper_2110_10548_b200 import executor

@@ -1,3 +1,6 @@
+"""Diagnostic: NVLS bf16 AllReduce on 2 GPUs against the single-rounded
+ordered sum, printing the elements that differ (the switch's bf16 reduction
+is not correctly rounded; profiles/r01_nvls_bf16_n2_rounding.txt)."""
 import os, sys, numpy as np
 sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
 os.environ["RS_NVLS"] = "1"
