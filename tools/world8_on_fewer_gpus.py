@@ -28,6 +28,8 @@ def main():
     K, progs = golden_programs("k8_sock")
     assert K == world == 8
     ctx = executor.Context.from_process_group(K, list(range(K)), 8 << 20)
+    if ctx.nvls:  # RS_NVLS=1: two ranks per GPU cannot share a multicast object -> consistent P2P fallback
+        ctx.set_option("nvls_min_bytes", 0)
     bad = 0
     cases = [(4097, numeric.F32, 0, -1), (3001, numeric.BF16, 256 << 10, -1), ((1 << 20) - 3, numeric.I32, 0, 0)]
     for N, dt, ll, push in cases:
@@ -49,7 +51,8 @@ def main():
     t = torch.tensor([bad])
     dist.all_reduce(t)
     if rank == 0:
-        print(f"world {world} on {torch.cuda.device_count()} GPUs: mismatches={int(t.item())}", flush=True)
+        print(f"world {world} on {torch.cuda.device_count()} GPUs (RS_NVLS={os.environ.get('RS_NVLS', '0')}, "
+              f"nvls after compiles: {ctx.nvls}): mismatches={int(t.item())}", flush=True)
     ctx.close()
     dist.destroy_process_group()
     return 0 if int(t.item()) == 0 else 1
