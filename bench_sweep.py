@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--min-bytes", dest="min", type=int, default=1 << 10)
     ap.add_argument("--max-bytes", dest="max", type=int, default=1 << 30)
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--step", type=int, default=2, help="size multiplier between rows")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--programs", default="all", help="'all' or 'first:N'")
     ap.add_argument("--out", default=None)
@@ -143,7 +144,7 @@ def main():
         if rank == 0:
             print(json.dumps({k: (round(v, 3) if isinstance(v, float) else v) for k, v in row.items()
                               if k != "programs"}), flush=True)
-        size *= 2
+        size *= args.step
     if rank == 0 and args.out:
         with open(args.out, "w") as f:
             json.dump({"K": K, "dtype": args.dtype, "descriptor": DESCRIPTORS[K], "rows": results}, f)
