@@ -193,6 +193,17 @@ def test_refusal_launches_nothing(local8):
     _run(local8, progs[0][2], K, 100, numeric.F32)
 
 
+def test_plan_time_and_prediction(local8):
+    """rs_plan_time (device time of a run) and the calibrated prediction
+    agree within a factor of two on a full-size config-2 program."""
+    K, progs = golden_programs("cfg2_r01")
+    plan = local8.compile(progs[0][2], 128 * 1024 * 1024, "bf16")
+    us = plan.time_us(1, 3)
+    pred = plan.predict_us(3.0, 650.0, 5967.0)
+    assert us > 0 and 0.5 < us / pred < 2.0, (us, pred)
+    plan.close()
+
+
 def test_oversize_refused(local8):
     K, progs = golden_programs("cfg1")
     with pytest.raises(ExecError) as e:
