@@ -121,7 +121,8 @@ class Context {
   uint64_t nvls_min_bytes = ~0ull;
   uint64_t nvls_min_bytes_n8 = 16ull << 20;
   // One-shot (LL) steps: when every cross-GPU group of a step has its members
-  // on distinct GPUs and each GPU sends any peer at most ll_max_bytes, the
+  // on distinct GPUs and each GPU sends any peer at most ll_max_bytes (and
+  // at most 3 * ll_max_bytes in total), the
   // step runs as one kernel in which every owner receives its sources as
   // flagged packets pushed into its own LL area and sums locally: no remote
   // loads, no tail wait (latency-bound sizes). ll_capacity is fixed at
