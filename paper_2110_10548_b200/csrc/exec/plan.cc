@@ -400,8 +400,9 @@ struct Compiler {
           owners[m] = m;
           parts[m] = geo.Ranges(std::vector<int>(rows.begin() + m * run, rows.begin() + (m + 1) * run));
         }
-        Sums(out, g, owners, parts, PushSums(g, TotalBytes(geo.Ranges(rows))),
-             [&](size_t j) { return std::vector<Ref>{Buf(g[j])}; });
+        // Pull only: measured faster than push for ReduceScatter at K=2 and
+        // K=4 up to 1 GiB (profiles/r01_collectives_vs_nccl.txt).
+        Sums(out, g, owners, parts, /*push=*/false, [&](size_t j) { return std::vector<Ref>{Buf(g[j])}; });
         for (int m = 0; m < n; ++m)
           for (int i = m * run; i < (m + 1) * run; ++i) Vid(g[m], rows[i]) = next_id++;
         break;
@@ -409,9 +410,20 @@ struct Compiler {
       case Collective::kReduce: {
         const std::vector<int> rows = HeldRows(pre, g[0]);
         const std::vector<Range> ranges = geo.Ranges(rows);
+        // n = 2: the root pulls the other member's data and sums locally —
+        // the link carries c one way only (non-root owners would move c both
+        // ways and leave all the work to one GPU). n >= 3: the non-roots own
+        // slices, so every GPU moves ~c per direction. Pull only (measured
+        // faster than push, profiles/r01_collectives_vs_nccl.txt).
+        // (Tried for n >= 3: every member owning a slice, root included —
+        // no faster; push — slower.)
         std::vector<int> owners;
-        for (int i = 1; i < n; ++i) owners.push_back(i);
-        Sums(out, g, owners, SplitEven(ranges, n - 1), PushSums(g, TotalBytes(ranges)),
+        if (n == 2) {
+          owners.push_back(0);
+        } else {
+          for (int i = 1; i < n; ++i) owners.push_back(i);
+        }
+        Sums(out, g, owners, SplitEven(ranges, static_cast<int>(owners.size())), /*push=*/false,
              [&](size_t) { return std::vector<Ref>{Buf(g[0])}; });
         for (int r : rows) Vid(g[0], r) = next_id++;
         break;

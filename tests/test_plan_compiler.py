@@ -80,13 +80,15 @@ def test_push_variant_every_program_bit_exact(name, mapping):
     """Push variant between two GPUs (one launch: sources land the owners'
     parts in their scratch chunk by chunk behind flags, owners reduce each
     landed chunk and push the results): same bits as the oracle,
-    hazard-free, and no vector task reads memory of another GPU (only
-    < 16-byte edges pull)."""
+    hazard-free, and in AllReduce / AllGather / Broadcast steps no vector
+    task reads memory of another GPU (only < 16-byte edges pull)."""
     K, progs = golden_programs(name)
     for _, _, prog, _ in progs[:: 2 if name.startswith("cfg2") else 1]:
         desc = _check(prog, K, mapping, 517, numeric.BF16, push=True)
         assert desc["num_phases"] == len(prog.steps)  # one launch per step
-        for step in desc["steps"]:
+        for step, (op, _) in zip(desc["steps"], prog.steps):
+            if op in (1, 3):  # ReduceScatter / Reduce always pull (measured faster)
+                continue
             for r, rk in enumerate(step["ranks"]):
                 for t in rk["tasks"]:
                     if t["vec"]:
@@ -397,3 +399,18 @@ def test_random_slot_to_gpu_mappings(seed):
                 simulate_plan(desc, got, dtype)
                 for d in range(K):
                     assert np.array_equal(got[d].view(np.uint8), want[d].view(np.uint8)), (prog.text, slot_rank, d)
+
+
+def test_two_member_reduce_is_pulled_by_the_root():
+    """Reduce over 2 GPUs: the root pulls the other member's data and sums
+    locally, so the link carries D one way only; wider groups keep
+    non-root owners (~D per direction on every GPU)."""
+    from paper_2110_10548_b200.planner import LoweredProgram
+    ctx = executor.Context.virtual(2, [0, 1], 2)
+    ctx.set_option("ll_max_bytes", 0)
+    plan = ctx.compile(LoweredProgram(steps=[(3, [[0, 1]])]), 1 << 20, "f32")
+    desc = plan.describe()
+    assert desc["steps"][0]["ranks"][1]["tasks"] == []
+    assert all(t["dst"] == [0] and t["src"] == [0, 1] for t in desc["steps"][0]["ranks"][0]["tasks"])
+    rk0, rk1 = desc["steps"][0]["ranks"]
+    assert rk0["rx"] == 4 << 20 and rk0["tx"] == 0 and rk1["tx"] == 4 << 20
