@@ -240,6 +240,12 @@ struct Compiler {
         if (m != h && Vid(m, r) != Vid(h, r)) recv.push_back(m);
       if (!recv.empty()) by_key[{h, recv}].push_back(r);
     }
+    // Push only balanced gathers (several holders, e.g. AllGather after a
+    // ReduceScatter); a one-to-all copy (Broadcast, AllGather after a Reduce)
+    // pulls: measured 15-25 % faster at K=2/K=4 from 128 MiB
+    // (profiles/r01_copies_push_vs_pull.txt).
+    std::set<int> holders;
+    for (auto [r, h] : row_holder) holders.insert(h);
     for (auto& [key, rows] : by_key) {
       const int h = key.first;
       const std::vector<int>& recv = key.second;
@@ -247,7 +253,7 @@ struct Compiler {
       const std::vector<Range> ranges = geo.Ranges(rows);
       std::vector<int> all = recv;
       all.push_back(h);
-      const bool push = PushCopies(all, TotalBytes(ranges));
+      const bool push = holders.size() > 1 && PushCopies(all, TotalBytes(ranges));
       const std::vector<std::vector<Range>> parts = SplitEven(ranges, static_cast<int>(recv.size()));
       for (size_t j = 0; j < recv.size(); ++j) {
         if (parts[j].empty()) continue;

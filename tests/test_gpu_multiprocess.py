@@ -125,12 +125,12 @@ def _worker(rank, world, port, result_dir):
         ctx.set_option("ll_max_bytes", 0)
         N, dt = (1 << 20) - 5, numeric.I32
         inputs = numeric.synthetic_inputs(K, N, dt)
+        pushed = 0
         for _, _, prog, _ in progs[:6]:
             ctx.write(rank, inputs[rank])
             plan = ctx.compile(prog, N, dt)
             modes = {t["mode"] for st in plan.describe()["steps"] for rk in st["ranks"] for t in rk["tasks"]}
-            if 3 not in modes:
-                raise AssertionError(f"expected push landing tasks: {prog.text}")
+            pushed += 3 in modes  # AllReduce / balanced AllGather steps push
             torch.cuda.synchronize()
             dist.barrier()
             g = torch.cuda.CUDAGraph()
@@ -151,6 +151,8 @@ def _worker(rank, world, port, result_dir):
             del g
             plan.close()
             dist.barrier()
+        if pushed == 0:
+            raise AssertionError("no program used the push variant")
         ctx.close()
         dist.destroy_process_group()
     except Exception:

@@ -80,14 +80,14 @@ def test_push_variant_every_program_bit_exact(name, mapping):
     """Push variant between two GPUs (one launch: sources land the owners'
     parts in their scratch chunk by chunk behind flags, owners reduce each
     landed chunk and push the results): same bits as the oracle,
-    hazard-free, and in AllReduce / AllGather / Broadcast steps no vector
-    task reads memory of another GPU (only < 16-byte edges pull)."""
+    hazard-free, and in AllReduce steps no vector task reads memory of
+    another GPU (only < 16-byte edges pull)."""
     K, progs = golden_programs(name)
     for _, _, prog, _ in progs[:: 2 if name.startswith("cfg2") else 1]:
         desc = _check(prog, K, mapping, 517, numeric.BF16, push=True)
         assert desc["num_phases"] == len(prog.steps)  # one launch per step
         for step, (op, _) in zip(desc["steps"], prog.steps):
-            if op in (1, 3):  # ReduceScatter / Reduce always pull (measured faster)
+            if op != 0:  # RS / Reduce / one-to-all copies pull (measured faster)
                 continue
             for r, rk in enumerate(step["ranks"]):
                 for t in rk["tasks"]:
@@ -414,3 +414,16 @@ def test_two_member_reduce_is_pulled_by_the_root():
     assert all(t["dst"] == [0] and t["src"] == [0, 1] for t in desc["steps"][0]["ranks"][0]["tasks"])
     rk0, rk1 = desc["steps"][0]["ranks"]
     assert rk0["rx"] == 4 << 20 and rk0["tx"] == 0 and rk1["tx"] == 4 << 20
+
+
+def test_copies_push_only_when_balanced():
+    """AllGather after a ReduceScatter (every member holds a run) pushes;
+    AllGather / Broadcast from a single holder (after a Reduce) pulls."""
+    K, progs = golden_programs("k2_flat")
+    rs_ag = next(p for _, _, p, _ in progs if p.text.startswith("Slice(root) InsideGroup ReduceScatter"))
+    red_bc = next(p for _, _, p, _ in progs if p.text.endswith("Broadcast"))
+    _, _, d1 = _compile(rs_ag, K, "one_per_gpu", 1 << 20, numeric.F32, push=True)
+    _, _, d2 = _compile(red_bc, K, "one_per_gpu", 1 << 20, numeric.F32, push=True)
+    modes = lambda d, s: {t["mode"] for rk in d["steps"][s]["ranks"] for t in rk["tasks"]}  # noqa: E731
+    assert 3 in modes(d1, 1)
+    assert modes(d2, 1) <= {0}
