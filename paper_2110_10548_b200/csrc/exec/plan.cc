@@ -421,8 +421,9 @@ struct Compiler {
         // ways and leave all the work to one GPU). n >= 3: the non-roots own
         // slices, so every GPU moves ~c per direction. Pull only (measured
         // faster than push, profiles/r01_collectives_vs_nccl.txt).
-        // (Tried for n >= 3: every member owning a slice, root included —
-        // no faster; push — slower.)
+        // (Tried for n >= 3: every member owning a slice, root included — no
+        // faster; push — slower; owners summing into their scratch behind
+        // chunk flags with the root pulling the results — slower.)
         std::vector<int> owners;
         if (n == 2) {
           owners.push_back(0);
@@ -519,11 +520,11 @@ void LayFlagged(RankStep& rs, const ProtoTask& t, uint64_t chunk) {
     task.hi = b;
     task.piece_begin = rs.npieces;
     task.ptr_begin = static_cast<uint32_t>(rs.ptr_refs.size());
-    task.nsrc = 1;
+    task.nsrc = static_cast<uint16_t>(t.src.size());
     task.ndst = 1;
     task.vec = 1;
     task.mode = kModeFlagSend;
-    rs.ptr_refs.push_back(t.src[0]);
+    rs.ptr_refs.insert(rs.ptr_refs.end(), t.src.begin(), t.src.end());
     rs.ptr_refs.push_back(t.dst[0]);
     rs.ptr_refs.push_back(FlagRef(t.flag_send));
     rs.npieces += static_cast<uint32_t>((b - a + chunk - 1) / chunk);
@@ -565,8 +566,8 @@ bool PlaceFlags(const Context& ctx, std::vector<RankStep>& phase) {
   for (int r = 0; r < ctx.world; ++r) {
     for (const Task& t : phase[r].tasks) {
       if (t.mode != kModeFlagSend) continue;
-      const Ref& dst = phase[r].ptr_refs[t.ptr_begin + 1];
-      const int id = phase[r].ptr_refs[t.ptr_begin + 2].slot;
+      const Ref& dst = phase[r].ptr_refs[t.ptr_begin + t.nsrc];
+      const int id = phase[r].ptr_refs[t.ptr_begin + t.nsrc + t.ndst].slot;
       const int owner_rank = ctx.slot_rank[dst.slot];
       const uint64_t chunks = (t.hi - t.lo + ctx.flag_chunk - 1) / ctx.flag_chunk;
       where[id] = {owner_rank, cursor[owner_rank]};
