@@ -32,7 +32,12 @@ namespace {
 
 __device__ __forceinline__ uint4 LoadStream(const void* p) {
   uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+#ifndef RS_LOAD_QUAL
+// 256-byte L2 prefetch on the streaming loads: +1-2 % on one GPU (2,803-2,830
+// vs 2,783 GB/s config 2), neutral over NVLink (profiles/r01_l2_prefetch_ab.txt).
+#define RS_LOAD_QUAL ".L1::no_allocate.L2::256B"
+#endif
+  asm volatile("ld.global.nc" RS_LOAD_QUAL ".v4.u32 {%0, %1, %2, %3}, [%4];"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p));
   return v;
