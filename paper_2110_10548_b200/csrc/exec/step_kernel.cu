@@ -33,8 +33,8 @@ namespace {
 __device__ __forceinline__ uint4 LoadStream(const void* p) {
   uint4 v;
 #ifndef RS_LOAD_QUAL
-// 256-byte L2 prefetch on the streaming loads: +1-2 % on one GPU (2,803-2,830
-// vs 2,783 GB/s config 2), neutral over NVLink (profiles/r01_l2_prefetch_ab.txt).
+// 256-byte L2 prefetch on the streaming loads: neutral to +2 % on one GPU
+// depending on the box, neutral over NVLink (profiles/r01_l2_prefetch_ab.txt).
 #define RS_LOAD_QUAL ".L1::no_allocate.L2::256B"
 #endif
   asm volatile("ld.global.nc" RS_LOAD_QUAL ".v4.u32 {%0, %1, %2, %3}, [%4];"
