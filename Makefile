@@ -25,7 +25,7 @@ EXEC_HDRS    := $(wildcard $(PKG)/csrc/exec/*.h) $(wildcard $(PKG)/csrc/exec/*.c
 EXEC_OBJS    := $(patsubst $(PKG)/csrc/exec/%.cc,$(LIB)/obj/exec_%.o,$(EXEC_CC)) \
                 $(patsubst $(PKG)/csrc/exec/%.cu,$(LIB)/obj/cu_%.o,$(EXEC_CU))
 
-.PHONY: all planner exec oracle check-ref clean
+.PHONY: all planner exec oracle check-ref clean profiling
 all: planner exec $(LIB)/synth $(LIB)/execute_example
 
 planner: $(LIB)/libredsynth_planner.a
@@ -52,6 +52,23 @@ $(LIB)/obj/cu_%.o: $(PKG)/csrc/exec/%.cu $(EXEC_HDRS)
 	$(NVCC) $(NVFLAGS) $(INC) -c $< -o $@ 2> $(LIB)/obj/cu_$*.ptxas.txt || (cat $(LIB)/obj/cu_$*.ptxas.txt; false)
 
 $(LIB)/libredsynth_b200.so: $(EXEC_OBJS) $(PLANNER_OBJS)
+	$(NVCC) -ccbin /usr/bin/g++ $(ARCH) -shared -o $@ $^ -Xcompiler -pthread
+
+# Profiling build (never loaded by default): the same library compiled with
+# RS_PROFILING_AIDS, which adds the RS_SOLO_PROFILE switch (no cross-GPU
+# waits, garbage data) used by tools/profile_p2p.py to replay one GPU's kernel
+# under ncu. Select it with RS_LIB_PATH=$(LIB)/libredsynth_b200_prof.so.
+profiling: $(LIB)/libredsynth_b200_prof.so
+
+$(LIB)/prof/exec_%.o: $(PKG)/csrc/exec/%.cc $(EXEC_HDRS)
+	@mkdir -p $(LIB)/prof
+	$(CXX) $(CXXFLAGS) -DRS_PROFILING_AIDS $(INC) $(CUDA_INC) -c $< -o $@
+
+$(LIB)/prof/cu_%.o: $(PKG)/csrc/exec/%.cu $(EXEC_HDRS)
+	@mkdir -p $(LIB)/prof
+	$(NVCC) $(NVFLAGS) -DRS_PROFILING_AIDS $(INC) -c $< -o $@ 2> $(LIB)/prof/cu_$*.ptxas.txt || (cat $(LIB)/prof/cu_$*.ptxas.txt; false)
+
+$(LIB)/libredsynth_b200_prof.so: $(patsubst $(LIB)/obj/%,$(LIB)/prof/%,$(filter $(LIB)/obj/exec_% $(LIB)/obj/cu_%,$(EXEC_OBJS))) $(PLANNER_OBJS)
 	$(NVCC) -ccbin /usr/bin/g++ $(ARCH) -shared -o $@ $^ -Xcompiler -pthread
 
 $(LIB)/execute_example: examples/execute_program.cc $(LIB)/libredsynth_b200.so

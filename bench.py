@@ -154,23 +154,91 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def bench_config(workload, world, n_programs):
+    """The `config` object of both arms (identical for the same workload)."""
+    if workload == "config2":
+        text = ("config 2: all 754 synthesized programs (axes [2,4] on b200_sock, reduce {1} "
+                "and {0,1}), 8 slots x 256 MiB bf16")
+    else:
+        text = (f"config 4 K={K_SLOTS}: all {n_programs} programs of {os.path.basename(SYSTEM)} axes {AXES}, "
+                f"{K_SLOTS} slots x 256 MiB bf16")
+    return {"workload": text, "slots_per_gpu": K_SLOTS // world, "programs": n_programs,
+            "parallelism": f"{world} GPU(s), slots block-distributed",
+            "l2": "inputs larger than L2 (8 x 256 MiB)"}
+
+
+class _Prog:
+    """A lowered program as the oracle reads it (steps of (op, groups))."""
+
+    def __init__(self, doc):
+        self.text = doc["text"]
+        self.seconds = doc.get("seconds")
+        self.steps = [(s["op"], [list(g) for g in s["groups"]]) for s in doc["steps"]]
+
+
+def reference_programs():
+    """The workload's program set from the REFERENCE itself: the unmodified
+    reference library built by oracle/Makefile (oracle/_ref), else the golden
+    fixtures it generated (tests/golden/programs_cfg2_*.json). Never from
+    this repository's planner."""
+    from oracle import ref
+    out = []
+    if ref.available():
+        with open(SYSTEM) as f:
+            system = f.read()
+        docs = [ref.synthesize(system, AXES, red, payload_bytes=D_BYTES) for red in REQUESTS]
+        source = "oracle/_ref (reference Synthesize)"
+    else:
+        names = {(1,): "cfg2_r1", (0, 1): "cfg2_r01"}
+        docs = []
+        for red in REQUESTS:
+            with open(os.path.join(ROOT, "tests", "golden", f"programs_{names[tuple(red)]}.json")) as f:
+                docs.append(json.load(f))
+        source = "tests/golden (reference Synthesize fixtures)"
+    for red, doc in zip(REQUESTS, docs):
+        for mi, m in enumerate(doc["matrices"]):
+            for pi, p in enumerate(m["programs"]):
+                out.append({"request": red, "matrix": mi, "index": pi, "prog": _Prog(p),
+                            "group_size": len(m["partition"][0])})
+    return out, source
+
+
 def run_reference(args):
     """--impl reference: the reference CPU path for this workload = the C
-    numeric oracle (a restatement of semantics.cc:259-310; the reference's
-    own RunLowered is symbolic and moves no data), all host threads, one
-    full-size config-2 program per step from a fixed sample."""
+    numeric oracle (a restatement of semantics.cc:259-310 folded as
+    dsl.cc:142-164; the reference's own RunLowered is symbolic and moves no
+    data) on all host threads, over the reference's own program set. Each
+    step executes one full-size program of the set (a spread over all 754,
+    in order), so the run stays bounded. Touches nothing of this
+    repository's package."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import numpy as np
+    if args.workload != "config2":
+        print(json.dumps({"impl": "reference", "unavailable": "reference arm is defined for config2 only"}))
+        return
+    import numpy as np  # noqa: F401
     from oracle import numeric, ref
-    progs = programs()
-    sample = [progs[i] for i in range(0, len(progs), max(1, len(progs) // 8))][:8]
+    progs, source = reference_programs()
+    total = args.warmup + args.steps
+    stride = max(1, len(progs) // max(1, total))
+    order = [progs[(i * stride) % len(progs)] for i in range(total)]
     threads = numeric.hardware_threads()
     inputs = numeric.synthetic_inputs(K_SLOTS, ELEMS, numeric.BF16)
     times, bytes_ = [], []
-    for it in range(args.warmup + args.steps):
-        e = sample[it % len(sample)]
+    for it, e in enumerate(order):
         bufs = [x.copy() for x in inputs]
         t0 = time.perf_counter()
         numeric.execute(e["prog"], K_SLOTS, bufs, numeric.BF16, nthreads=threads)
@@ -181,16 +249,18 @@ def run_reference(args):
     value = sum(bytes_) / sum(times) / 1e9
     symbolic_us = None
     if ref.available():
-        symbolic_us = statistics.mean(ref.time_run_lowered(e["prog"].steps, K_SLOTS, 2000) for e in sample)
+        symbolic_us = statistics.mean(ref.time_run_lowered(e["prog"].steps, K_SLOTS, 2000) for e in order)
+    sample = (f"{args.steps} timed programs (after {args.warmup} warm-up), one per step: every {stride}th of the "
+              f"{len(progs)} programs from {source}, each at full size (8 x 256 MiB bf16)")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * sum(times) / len(times), 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "config 2 sample: one full-size program (8 slots x 256 MiB bf16) per step",
-                   "programs_in_sample": len(sample)},
-        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"{len(sample)} config-2 programs at full size, one per step"},
+        "config": bench_config("config2", args.gpus, len(progs)),
+        "reference_sample": sample,
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "cpu_model": cpu_model(),
+                         "kind": "port", "sample": sample},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "reference_runlowered_us_per_program": symbolic_us,
     }
@@ -547,13 +617,7 @@ def main():
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": ("config 2: all 754 synthesized programs (axes [2,4] on b200_sock, reduce {1} "
-                                    "and {0,1}), 8 slots x 256 MiB bf16") if args.workload == "config2" else
-                                   (f"config 4 K={K_SLOTS}: all {len(entries)} programs of "
-                                    f"{os.path.basename(SYSTEM)} axes {AXES}, {K_SLOTS} slots x 256 MiB bf16"),
-                       "slots_per_gpu": K_SLOTS // world, "programs": len(entries),
-                       "parallelism": f"{world} GPU(s), slots block-distributed",
-                       "l2": "inputs larger than L2 (8 x 256 MiB)"},
+            "config": bench_config(args.workload, world, len(entries)),
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -600,7 +664,8 @@ def cpu_baseline(entries):
         t += time.perf_counter() - t0
         b += bus_bytes(e)
         done += 1
-    return {"value": round(b / t / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+    return {"value": round(b / t / 1e9, 3), "unit": "GB/s", "cores": threads, "cpu_model": cpu_model(),
+            "kind": "port",
             "sample": f"{done} config-2 programs (every 97th of the 754, in order) at full size "
                       f"(8 x 256 MiB bf16), ~10 s of CPU time",
             "seconds": round(t, 2)}

@@ -331,19 +331,26 @@ absl::Status OpenPeers(Context* ctx, const void* handles) {
 }
 
 absl::Status Synchronize(Context* ctx) {
+  // Plans usually run on caller streams (rs_plan_run streams, torch's current
+  // stream), so wait for the whole device, not just the context's streams.
+  // The timeout flag is reported once and then cleared, so later healthy
+  // runs synchronize cleanly.
+  absl::Status first = absl::OkStatus();
   for (int r : ctx->DrivenRanks()) {
     Rank& rank = ctx->ranks[r];
     RS_CUDA(cudaSetDevice(rank.ordinal));
-    RS_CUDA(cudaStreamSynchronize(rank.stream));
+    RS_CUDA(cudaDeviceSynchronize());
     int err = 0;
     RS_CUDA(cudaMemcpy(&err, rank.heap + kErrorOffset, sizeof(int), cudaMemcpyDeviceToHost));
     if (err) {
-      return absl::InternalError(absl::StrFormat(
-          "rank %d: inter-GPU barrier timed out (a peer never reached the step); results are invalid",
-          r));
+      RS_CUDA(cudaMemset(rank.heap + kErrorOffset, 0, sizeof(int)));
+      if (first.ok()) {
+        first = absl::InternalError(absl::StrFormat(
+            "rank %d: inter-GPU barrier timed out (a peer never reached the step); results are invalid", r));
+      }
     }
   }
-  return absl::OkStatus();
+  return first;
 }
 
 absl::Status DestroyContext(Context* ctx) {
@@ -435,6 +442,30 @@ absl::Status EnsureMulticast(Context* ctx, const std::vector<int>& slots, int* i
     ctx->mc_groups[slots] = std::move(mc);
     return absl::OkStatus();
   }
+  // Everything created below is released on every early return (a failed
+  // NVLS setup falls back to P2P and must not leak switch resources).
+  struct Cleanup {
+    McGroup* mc;
+    std::vector<std::pair<int, CUdevice>> bound;  // (ordinal, device) bound to mc
+    std::vector<std::pair<int, CUdeviceptr>> mapped;  // (ordinal, va)
+    int fd = -1;
+    bool armed = true;
+    ~Cleanup() {
+      if (fd >= 0) close(fd);
+      if (!armed) return;
+      for (auto [ord, va] : mapped) {
+        cudaSetDevice(ord);
+        drv::cuMemUnmap(va, mc->bytes);
+        drv::cuMemAddressFree(va, mc->bytes);
+      }
+      for (auto [ord, dev] : bound) {
+        cudaSetDevice(ord);
+        drv::cuMulticastUnbind(mc->handle, dev, 0, mc->bytes);
+      }
+      if (mc->handle) drv::cuMemRelease(mc->handle);
+      std::fill(mc->va.begin(), mc->va.end(), 0);
+    }
+  } guard{mc.get()};
   const int n = static_cast<int>(slots.size());
   const size_t gran = MulticastGranularity(n, ctx->max_bytes);
   mc->bytes = (ctx->max_bytes + gran - 1) / gran * gran;
@@ -453,13 +484,21 @@ absl::Status EnsureMulticast(Context* ctx, const std::vector<int>& slots, int* i
     absl::Status s = CuStatus(
         drv::cuMulticastBindMem(mc->handle, 0, ctx->ranks[r].vmm.handle, ctx->SlotOffset(slot, -1), mc->bytes, 0),
         "cuMulticastBindMem");
+    if (s.ok()) guard.bound.push_back({ctx->ranks[r].ordinal, device_of(r)});
     return s;
   };
   auto map_va = [&](const std::vector<int>& access, CUdeviceptr* va) -> absl::Status {
     absl::Status s = CuStatus(drv::cuMemAddressReserve(va, mc->bytes, gran, 0, 0), "reserve multicast VA");
     if (!s.ok()) return s;
     s = CuStatus(drv::cuMemMap(*va, mc->bytes, 0, mc->handle, 0), "map multicast VA");
-    if (!s.ok()) return s;
+    if (!s.ok()) {
+      drv::cuMemAddressFree(*va, mc->bytes);
+      *va = 0;
+      return s;
+    }
+    int ord = 0;
+    cudaGetDevice(&ord);
+    guard.mapped.push_back({ord, *va});
     std::vector<CUmemAccessDesc> desc(access.size());
     for (size_t i = 0; i < access.size(); ++i) {
       desc[i].location.type = CU_MEM_LOCATION_TYPE_DEVICE;
@@ -512,6 +551,7 @@ absl::Status EnsureMulticast(Context* ctx, const std::vector<int>& slots, int* i
         s = CuStatus(drv::cuMemExportToShareableHandle(&fd, mc->handle, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0),
                      "export multicast");
         mine = McShare{static_cast<int32_t>(getpid()), fd, s.ok() ? 1 : 0, 0};
+        guard.fd = fd;
       }
     }
     std::vector<char> all;
@@ -562,8 +602,8 @@ absl::Status EnsureMulticast(Context* ctx, const std::vector<int>& slots, int* i
       std::memcpy(&v, all.data() + r * sizeof(int32_t), sizeof(v));
       if (!v) return s.ok() ? absl::InternalError(absl::StrFormat("rank %d failed to bind multicast", r)) : s;
     }
-    if (me == creator && mine.fd >= 0) close(mine.fd);
   }
+  guard.armed = false;  // success: the context owns the group (DestroyContext releases it)
   *index = static_cast<int>(ctx->mc_index.size());
   ctx->mc_index.push_back(mc.get());
   ctx->mc_groups[slots] = std::move(mc);

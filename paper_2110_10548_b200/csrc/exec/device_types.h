@@ -75,7 +75,8 @@ struct StepArgs {
   uint64_t timeout_ns;
   uint64_t ll_parity_stride;  // bytes between the two parity regions of an LL block
   uint32_t flag_chunk;        // push-variant chunk (bytes per flag)
-  uint32_t solo;              // profiling aid (RS_SOLO_PROFILE): skip every cross-GPU wait
+  uint32_t local_only;        // single-rank context: sources are read-only for the launch (.nc loads)
+  uint32_t solo;              // profiling builds only (RS_PROFILING_AIDS): skip every cross-GPU wait
 };
 
 // Vector work is cut into pieces of kPieceBytes; a CTA walks a piece in

@@ -29,13 +29,17 @@ namespace rs {
 //                  rank, two parity regions of 2 * ll_capacity bytes (16-byte
 //                  packets {data0, flag, data1, flag} carry 8 payload bytes)
 //   then           push-variant chunk flags when world > 1: one uint64 per
-//                  64 KiB chunk of every hosted slot buffer and scratch region
+//                  flag_chunk (default kFlagChunk = 256 KiB) of every hosted
+//                  slot buffer and scratch region
 constexpr size_t kInboxOffset = 0;
 constexpr size_t kCounterOffset = 256;
 constexpr size_t kErrorOffset = 512;
 constexpr size_t kEpochOffset = 768;
 constexpr size_t kDataOffset = 2u << 20;  // multicast-bind granularity
 constexpr size_t kSlotAlign = 1 << 21;
+// Planning-only contexts and peers driven by other processes: SM count used
+// to size pieces when the device attribute is not at hand (B200).
+constexpr int kDefaultSmCount = 148;
 
 struct Rank {
   int ordinal = -1;         // CUDA device (meaningful for ranks driven here)
@@ -182,8 +186,8 @@ class Plan {
   int unroll = 4;      // 4 or 8 vectors in flight per thread per source
   int max_ctas = 0;    // 0 = resident capacity
   int ctas_per_sm = 0;  // resident capacity for (dtype, threads, unroll); 0 = recompute
-  // Launch phases: a program step is one phase (pull variant) or two (push
-  // variant: scatter into owners' scratch, then reduce + push results).
+  // Launch phases, one per program step (every variant — pull, push with
+  // chunk flags, one-shot, NVLS — runs its step in a single launch).
   std::vector<std::vector<RankStep>> phases;  // [phase][rank]
   std::vector<int> phase_step;                // program step of each phase
   std::vector<uint8_t> phase_ll;              // 1: one-shot (LL) phase

@@ -931,8 +931,9 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
     std::vector<uint64_t> rank_bytes(R, 0);
     for (const ProtoTask& t : list) rank_bytes[ctx->slot_rank[t.owner]] += t.range.hi - t.range.lo;
     for (int r = 0; r < R; ++r) {
+      const uint64_t sms = ctx->ranks[r].sm_count > 0 ? ctx->ranks[r].sm_count : kDefaultSmCount;
       uint32_t pb = 4u << 10;
-      while (pb < kPieceBytes && rank_bytes[r] / pb > 2 * 148) pb <<= 1;
+      while (pb < kPieceBytes && rank_bytes[r] / pb > 2 * sms) pb <<= 1;
       plan->phases.back()[r].piece_bytes = pb;
     }
     for (const ProtoTask& t : list) {

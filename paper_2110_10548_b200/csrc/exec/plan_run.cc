@@ -23,8 +23,10 @@ Plan::~Plan() {
 // (the per-run host path is then one launch per record).
 void BuildLaunches(Plan* plan) {
   Context* ctx = plan->ctx;
+#ifdef RS_PROFILING_AIDS
   const char* solo_env = std::getenv("RS_SOLO_PROFILE");
   const bool solo = solo_env && std::atoi(solo_env) != 0;
+#endif
   const int P = plan->num_phases();
   const int R = ctx->world;
   plan->launch_args.assign(static_cast<size_t>(P) * R, StepArgs{});
@@ -57,14 +59,18 @@ void BuildLaunches(Plan* plan) {
             if (plan->final_wait_bits[r] & (1u << q)) a.final_ranks[a.nfinal++] = static_cast<uint8_t>(q);
         }
       }
+#ifdef RS_PROFILING_AIDS
       if (solo) {
-        // Profiling aid (RS_SOLO_PROFILE=1): no cross-GPU waits, so ncu can
-        // replay one GPU's pull/push kernel alone and count its NVLink bytes
-        // (results are garbage; never set in production).
+        // Profiling builds only (make profiling -> libredsynth_b200_prof.so):
+        // with RS_SOLO_PROFILE=1 no cross-GPU waits, so ncu can replay one
+        // GPU's pull/push kernel alone and count its NVLink bytes (results
+        // are garbage). The release library has no such switch.
         a.nwait = 0;
         a.nfinal = 0;
         a.solo = 1;
       }
+#endif
+      a.local_only = ctx->world == 1 ? 1u : 0u;
       a.signal_done = rsx.signal_done ? 1u : 0u;
       a.wait_lag = static_cast<uint32_t>(plan->phase_lag[ph]);
       a.epoch_base = reinterpret_cast<uint64_t*>(rank.heap + kEpochOffset);
@@ -82,7 +88,7 @@ void BuildLaunches(Plan* plan) {
       // AllReduce, profiles/r01_tune4_push0.log); from one peer two per SM
       // are better (652 vs 637 at K=2, r01_tune_n2.log).
       if (plan->max_ctas == 0 && !a.has_nvls && !a.has_ll && rsx.remote_peers >= 2) cap = std::min(cap, rank.sm_count);
-      if (cap <= 0) cap = 148;
+      if (cap <= 0) cap = std::max(1, rank.sm_count);
       plan->launch_grid[static_cast<size_t>(ph) * R + r] = std::max(1, std::min<int>(cap, static_cast<int>(rsx.npieces)));
     }
   }
@@ -202,7 +208,7 @@ std::string DescribePlan(const Plan& plan) {
     }
     phases.push_back({{"ranks", ranks}});
   }
-  doc["steps"] = std::move(phases);  // launch phases (== program steps without push)
+  doc["steps"] = std::move(phases);  // launch phases: one per program step
   std::vector<std::vector<int>> final_wait;
   for (uint8_t bits : plan.final_wait_bits) {
     std::vector<int> w;

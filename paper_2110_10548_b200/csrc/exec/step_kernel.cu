@@ -16,7 +16,8 @@
 // Small steps run one-shot (LL): every destination sums its own result from
 // flagged 16-byte packets its sources pushed into its LL area (kModeLL).
 // Large AllReduce groups on >= 4 GPUs may use NVLS multimem instead.
-// Memory: 16-byte vector loads (ld.global.nc.L1::no_allocate) and streaming
+// Memory: 16-byte vector loads (ld.global.nc.L1::no_allocate on one GPU,
+// weak ld.global.L1::no_allocate across GPUs) and streaming
 // stores, 4 (cross-GPU) or 8 (one GPU) vectors in flight per thread per
 // source, coalesced 512 B per warp.
 // Inter-GPU ordering: epoch flags in each rank's heap (relaxed st.sys behind
@@ -30,6 +31,14 @@
 namespace rs {
 namespace {
 
+// Streaming 16-byte load. The non-coherent (.nc) form is only legal for data
+// that is read-only for the kernel's whole lifetime: true in a single-rank
+// context (every step of a local plan is hazard-free and nobody else writes
+// the heap), not across GPUs, where a peer may write a slot buffer (previous
+// step's results) while this kernel waits at its entry barrier. Cross-rank
+// launches therefore use weak ld.global (ordered after the entry acquire by
+// the CTA barrier), still without L1 allocation.
+template <bool kNc>
 __device__ __forceinline__ uint4 LoadStream(const void* p) {
   uint4 v;
 #ifndef RS_LOAD_QUAL
@@ -37,9 +46,16 @@ __device__ __forceinline__ uint4 LoadStream(const void* p) {
 // depending on the box, neutral over NVLink (profiles/r01_l2_prefetch_ab.txt).
 #define RS_LOAD_QUAL ".L1::no_allocate.L2::256B"
 #endif
-  asm volatile("ld.global.nc" RS_LOAD_QUAL ".v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p));
+  if constexpr (kNc) {
+    asm volatile("ld.global.nc" RS_LOAD_QUAL ".v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+  } else {
+    asm volatile("ld.global" RS_LOAD_QUAL ".v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+  }
   return v;
 }
 
@@ -97,16 +113,24 @@ __device__ __forceinline__ uint64_t GlobalTimer() {
   return t;
 }
 
+__device__ __forceinline__ bool Failed(const int* error_flag) {
+  return *reinterpret_cast<const volatile int*>(error_flag) != 0;
+}
+
 // Spin until *flag >= target; on timeout raise the error flag and give up
 // (the data is then wrong, but the GPU is not hung; the host reports it).
+// Once this rank's error flag is up every later wait returns at once, so a
+// dead peer costs one timeout per run, not one per wait.
 __device__ void WaitAtLeast(const uint64_t* flag, uint64_t target, uint64_t timeout_ns,
                             int* error_flag) {
   // Tight spin first (a peer is usually < 2 us away), then back off.
   for (int i = 0; i < 4096; ++i) {
     if (LoadAcquireSys(flag) >= target) return;
   }
+  if (Failed(error_flag)) return;
   const uint64_t t0 = GlobalTimer();
   while (LoadAcquireSys(flag) < target) {
+    if (Failed(error_flag)) return;
     if (GlobalTimer() - t0 > timeout_ns) {
       atomicExch(error_flag, 1);
       return;
@@ -175,7 +199,7 @@ template <> struct AccOf<RS_I32> { using T = I32Acc; };
 
 // One block-wide chunk: bytes [begin, end) of the task, 16-byte aligned;
 // thread t handles vectors begin + (u * blockDim + t) * 16, u < kUnroll.
-template <int DT, int kUnroll, bool kCoherent = false>
+template <int DT, int kUnroll, bool kNc, bool kCoherent = false>
 __device__ __forceinline__ void VectorChunk(const Task& t, void* const* ptrs, uint64_t begin,
                                             uint64_t end) {
   using Acc = typename AccOf<DT>::T;
@@ -192,7 +216,7 @@ __device__ __forceinline__ void VectorChunk(const Task& t, void* const* ptrs, ui
   const char* s0 = static_cast<const char*>(src[0]);
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u)
-    if (ok[u]) raw[u] = kCoherent ? LoadCoherent(s0 + off[u]) : LoadStream(s0 + off[u]);
+    if (ok[u]) raw[u] = kCoherent ? LoadCoherent(s0 + off[u]) : LoadStream<kNc>(s0 + off[u]);
   if (t.nsrc > 1) {
     Acc acc[kUnroll];
 #pragma unroll
@@ -201,7 +225,7 @@ __device__ __forceinline__ void VectorChunk(const Task& t, void* const* ptrs, ui
       const char* si = static_cast<const char*>(src[i]);
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u)
-        if (ok[u]) raw[u] = kCoherent ? LoadCoherent(si + off[u]) : LoadStream(si + off[u]);
+        if (ok[u]) raw[u] = kCoherent ? LoadCoherent(si + off[u]) : LoadStream<kNc>(si + off[u]);
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) acc[u].Add(raw[u]);
     }
@@ -226,6 +250,7 @@ __device__ __forceinline__ void NvlsChunk(const Task& t, void* const* ptrs, uint
   uint4 v[kUnroll];
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u) {
+    v[u] = make_uint4(0, 0, 0, 0);  // defined on every path (no spills around the loads)
     const uint64_t off = begin + (static_cast<uint64_t>(u) * blockDim.x + threadIdx.x) * 16u;
     if (off >= end) continue;
     if constexpr (DT == RS_BF16) {
@@ -309,8 +334,11 @@ __device__ __forceinline__ uint2 LoadLL(const char* p, uint32_t flag, uint64_t t
                  : "l"(p)
                  : "memory");
     if (f0 == flag && f1 == flag) break;
-    if (spin == 4096) t0 = GlobalTimer();
-    if (spin > 4096 && (spin & 63) == 0 && GlobalTimer() - t0 > timeout_ns) {
+    if (spin == 4096) {
+      if (Failed(error_flag)) break;
+      t0 = GlobalTimer();
+    }
+    if (spin > 4096 && (spin & 63) == 0 && (Failed(error_flag) || GlobalTimer() - t0 > timeout_ns)) {
       atomicExch(error_flag, 1);
       break;
     }
@@ -566,7 +594,7 @@ __device__ __forceinline__ void LLReceive(const Task& t, void* const* ptrs, uint
 }
 
 // One launch phase of one rank: entry barrier, tasks, exit.
-template <int DT, int kUnroll, bool kLL>
+template <int DT, int kUnroll, bool kLL, bool kNc>
 __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
   // 1. First step of a run: publish "my inputs are in place" to every peer.
   if (a.step == 0 && blockIdx.x == 0 && threadIdx.x < a.nsignal) {
@@ -622,14 +650,20 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
       const uint64_t chunk = static_cast<uint64_t>(blockDim.x) * kUnroll * 16u;
       void* const* flags = a.ptrs + t.ptr_begin + t.nsrc + t.ndst;
       if (t.mode == kModeFlagRecv) {
-        if (threadIdx.x < t.nsrc && flags[threadIdx.x] && !a.solo) {
+#ifdef RS_PROFILING_AIDS
+        const bool skip_wait = a.solo != 0;
+#else
+        constexpr bool skip_wait = false;
+#endif
+        if (threadIdx.x < t.nsrc && flags[threadIdx.x] && !skip_wait) {
           WaitAtLeast(static_cast<const uint64_t*>(flags[threadIdx.x]) + k, epoch, a.timeout_ns, a.error_flag);
         }
         __syncthreads();
         for (uint64_t c = begin; c < end; c += chunk)
-          VectorChunk<DT, kUnroll, true>(t, a.ptrs, c, min(end, c + chunk));
+          VectorChunk<DT, kUnroll, kNc, true>(t, a.ptrs, c, min(end, c + chunk));
       } else {
-        for (uint64_t c = begin; c < end; c += chunk) VectorChunk<DT, kUnroll>(t, a.ptrs, c, min(end, c + chunk));
+        for (uint64_t c = begin; c < end; c += chunk)
+          VectorChunk<DT, kUnroll, kNc>(t, a.ptrs, c, min(end, c + chunk));
         __syncthreads();
         if (threadIdx.x == 0) {
           FenceSys();
@@ -648,7 +682,7 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
           continue;
         }
       }
-      for (uint64_t c = begin; c < end; c += chunk) VectorChunk<DT, kUnroll>(t, a.ptrs, c, min(end, c + chunk));
+      for (uint64_t c = begin; c < end; c += chunk) VectorChunk<DT, kUnroll, kNc>(t, a.ptrs, c, min(end, c + chunk));
     } else {
       ScalarTask<DT>(t, a.ptrs);
     }
@@ -687,11 +721,11 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
   }
 }
 
-template <int DT, int kUnroll, bool kLL>
+template <int DT, int kUnroll, bool kLL, bool kNc>
 __global__ void __launch_bounds__(512, kUnroll == 4 ? 2 : 1) StepKernel(const __grid_constant__ StepArgs a) {
   // Run base epoch (device resident; advanced by the previous run's last step).
   const uint64_t base = a.nsignal ? *reinterpret_cast<volatile uint64_t*>(a.epoch_base) : 0;
-  Phase<DT, kUnroll, kLL>(a, base);
+  Phase<DT, kUnroll, kLL, kNc>(a, base);
 }
 
 template <int U>
@@ -699,9 +733,9 @@ int Occupancy(int dtype, int threads) {
   int blocks = 0;
   cudaError_t e = cudaSuccess;
   switch (dtype) {
-    case RS_F32: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_F32, U, false>, threads, 0); break;
-    case RS_BF16: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_BF16, U, false>, threads, 0); break;
-    default: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_I32, U, false>, threads, 0); break;
+    case RS_F32: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_F32, U, false, false>, threads, 0); break;
+    case RS_BF16: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_BF16, U, false, false>, threads, 0); break;
+    default: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, StepKernel<RS_I32, U, false, false>, threads, 0); break;
   }
   if (e != cudaSuccess || blocks < 1) {
     cudaGetLastError();
@@ -710,12 +744,12 @@ int Occupancy(int dtype, int threads) {
   return blocks;
 }
 
-template <int U, bool LL>
+template <int U, bool LL, bool NC>
 cudaError_t Launch(const StepArgs& a, int grid, int block, cudaStream_t stream) {
   switch (a.dtype) {
-    case RS_F32: StepKernel<RS_F32, U, LL><<<grid, block, 0, stream>>>(a); break;
-    case RS_BF16: StepKernel<RS_BF16, U, LL><<<grid, block, 0, stream>>>(a); break;
-    case RS_I32: StepKernel<RS_I32, U, LL><<<grid, block, 0, stream>>>(a); break;
+    case RS_F32: StepKernel<RS_F32, U, LL, NC><<<grid, block, 0, stream>>>(a); break;
+    case RS_BF16: StepKernel<RS_BF16, U, LL, NC><<<grid, block, 0, stream>>>(a); break;
+    case RS_I32: StepKernel<RS_I32, U, LL, NC><<<grid, block, 0, stream>>>(a); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -728,8 +762,14 @@ int MaxResidentCtas(int dtype, int threads, int unroll) {
 }
 
 cudaError_t LaunchStep(const StepArgs& args, int grid, int block, int unroll, cudaStream_t stream) {
-  if (args.has_ll) return Launch<2, true>(args, grid, block, stream);  // (512, 1): 128 registers
-  return unroll == 8 ? Launch<8, false>(args, grid, block, stream) : Launch<4, false>(args, grid, block, stream);
+  // One-shot phases only exist across GPUs (never .nc); (512, 1): 128 registers.
+  if (args.has_ll) return Launch<2, true, false>(args, grid, block, stream);
+  if (args.local_only) {
+    return unroll == 8 ? Launch<8, false, true>(args, grid, block, stream)
+                       : Launch<4, false, true>(args, grid, block, stream);
+  }
+  return unroll == 8 ? Launch<8, false, false>(args, grid, block, stream)
+                     : Launch<4, false, false>(args, grid, block, stream);
 }
 
 }  // namespace rs

@@ -3,7 +3,8 @@
 per GPU): with RS_SOLO_PROFILE=1 the kernels skip their cross-GPU waits, so
 ncu (which serialises launches) can replay each GPU's kernel alone and count
 its NVLink bytes (nvltx/nvlrx) next to its DRAM bytes. The data is garbage in
-this mode — it only measures traffic.
+this mode — it only measures traffic. The switch exists only in the
+profiling build (`make profiling`), which this script selects itself.
 
   RS_SOLO_PROFILE=1 ncu --metrics gpu__time_duration.sum,nvltx__bytes.sum,nvlrx__bytes.sum,\
 dram__bytes_read.sum,dram__bytes_write.sum python tools/profile_p2p.py --gpus 2
@@ -27,6 +28,10 @@ def main():
     if os.environ.get("RS_SOLO_PROFILE") != "1":
         raise SystemExit("set RS_SOLO_PROFILE=1 (the kernels would wait for peers ncu never runs)")
     os.environ.setdefault("RS_BARRIER_TIMEOUT_S", "2")
+    prof = os.path.join(ROOT, "paper_2110_10548_b200", "_lib", "libredsynth_b200_prof.so")
+    if not os.path.exists(prof):
+        raise SystemExit("build the profiling library first: make profiling")
+    os.environ["RS_LIB_PATH"] = prof
     import torch
     from paper_2110_10548_b200 import executor, planner
     n = args.gpus
