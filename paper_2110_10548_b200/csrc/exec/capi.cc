@@ -260,8 +260,11 @@ int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value) {
     ctx->impl->nvls_min_bytes_n8 = ctx->impl->nvls_min_bytes;
   } else if (k == "ll_max_bytes") {
     ctx->impl->ll_max_bytes = value < 0 ? 0 : static_cast<uint64_t>(value);
+  } else if (k == "reduce_mode") {
+    if (value < rs::kReducePull || value > rs::kReduceNvlsRoot) return Bad("reduce_mode must be 0 (pull), 1 (push), 2 (nvls) or 3 (nvls root)");
+    ctx->impl->reduce_mode = static_cast<int>(value);
   } else {
-    return Bad("unknown option (push_min_bytes | barrier_timeout_ms | nvls | nvls_min_group | nvls_min_bytes | ll_max_bytes)");
+    return Bad("unknown option (push_min_bytes | barrier_timeout_ms | nvls | nvls_min_group | nvls_min_bytes | ll_max_bytes | reduce_mode)");
   }
   return RS_OK;
 }

@@ -151,6 +151,10 @@ void ReadTimeoutEnv(Context* ctx) {
     ctx->push_min_bytes = std::strtoull(env, nullptr, 10);
   }
   if (const char* env = std::getenv("RS_PUSH_MAX_GPUS")) ctx->push_max_gpus = std::atoi(env);
+  if (const char* env = std::getenv("RS_REDUCE_MODE")) {
+    const int m = std::atoi(env);
+    if (m >= kReducePull && m <= kReduceNvlsRoot) ctx->reduce_mode = m;
+  }
 }
 
 }  // namespace
@@ -417,6 +421,116 @@ absl::Status Exchange(Context* ctx, const void* send, size_t bytes, std::vector<
   return absl::OkStatus();
 }
 
+// NVLS self-check (every new multicast object, before any plan uses it):
+// each member's first kSelfCheckBytes are saved, filled with small integers
+// (exact f32 sums), all-reduced through the switch by the members (each its
+// slice, the instructions the NVLS tasks use), compared with the expected
+// sums and restored. Any failure — a launch error, a wrong sum, a rank that
+// cannot run it — makes every rank drop the object and fall back to P2P.
+constexpr size_t kSelfCheckBytes = 64u << 10;
+
+float SelfCheckValue(int slot, size_t e) { return static_cast<float>(slot % 5 + 1) + static_cast<float>(e % 7); }
+
+absl::Status NvlsSelfCheck(Context* ctx, McGroup* mc, const std::vector<int>& slots,
+                           absl::Status (*barrier)(Context*, int32_t ok, bool* all_ok)) {
+  const size_t elems = kSelfCheckBytes / sizeof(float);
+  const int n = static_cast<int>(slots.size());
+  std::vector<int> mine;  // indices into slots of the members driven here
+  for (int i = 0; i < n; ++i)
+    if (ctx->ranks[ctx->slot_rank[slots[i]]].driven) mine.push_back(i);
+  std::vector<void*> saved(mine.size(), nullptr);
+  int32_t ok = 1;
+  std::vector<float> host(elems);
+  bool all_ok = false;
+  // 0. quiesce: runs enqueued earlier (on any stream, by any rank) may still
+  //    touch the slot buffers
+  for (const Rank& rank : ctx->ranks) {
+    if (!rank.driven) continue;
+    ok &= cudaSetDevice(rank.ordinal) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess;
+  }
+  absl::Status bs = barrier(ctx, ok, &all_ok);
+  if (!bs.ok()) return bs;
+  // 1. save + fill
+  for (size_t k = 0; k < mine.size() && ok; ++k) {
+    const int d = slots[mine[k]];
+    const int r = ctx->slot_rank[d];
+    ok &= cudaSetDevice(ctx->ranks[r].ordinal) == cudaSuccess;
+    ok &= ok && cudaMalloc(&saved[k], kSelfCheckBytes) == cudaSuccess;
+    ok &= ok && cudaMemcpy(saved[k], ctx->SlotPtr(r, d), kSelfCheckBytes, cudaMemcpyDeviceToDevice) == cudaSuccess;
+    for (size_t e = 0; e < elems; ++e) host[e] = SelfCheckValue(d, e);
+    ok &= ok && cudaMemcpy(ctx->SlotPtr(r, d), host.data(), kSelfCheckBytes, cudaMemcpyHostToDevice) == cudaSuccess;
+    ok &= ok && cudaDeviceSynchronize() == cudaSuccess;
+  }
+  bs = barrier(ctx, ok, &all_ok);
+  if (!bs.ok()) return bs;
+  // 2. reduce through the switch: member i handles slice i
+  if (all_ok) {
+    for (size_t k = 0; k < mine.size() && ok; ++k) {
+      const int i = mine[k];
+      const int r = ctx->slot_rank[slots[i]];
+      const uint64_t lo = (kSelfCheckBytes * i / n) & ~uint64_t{15};
+      const uint64_t hi = i + 1 == n ? kSelfCheckBytes : (kSelfCheckBytes * (i + 1) / n) & ~uint64_t{15};
+      ok &= cudaSetDevice(ctx->ranks[r].ordinal) == cudaSuccess;
+      ok &= ok && LaunchNvlsSelfCheck(reinterpret_cast<char*>(mc->va[r]), lo, hi, nullptr) == cudaSuccess;
+    }
+    for (size_t k = 0; k < mine.size(); ++k) {
+      cudaSetDevice(ctx->ranks[ctx->slot_rank[slots[mine[k]]]].ordinal);
+      ok &= cudaDeviceSynchronize() == cudaSuccess;
+    }
+    bs = barrier(ctx, ok, &all_ok);
+    if (!bs.ok()) return bs;
+  }
+  // 3. compare
+  if (all_ok) {
+    for (size_t k = 0; k < mine.size() && ok; ++k) {
+      const int d = slots[mine[k]];
+      const int r = ctx->slot_rank[d];
+      cudaSetDevice(ctx->ranks[r].ordinal);
+      ok &= cudaMemcpy(host.data(), ctx->SlotPtr(r, d), kSelfCheckBytes, cudaMemcpyDeviceToHost) == cudaSuccess;
+      for (size_t e = 0; e < elems && ok; ++e) {
+        float want = 0;
+        for (int m : slots) want += SelfCheckValue(m, e);
+        ok &= host[e] == want;
+      }
+    }
+    bs = barrier(ctx, ok, &all_ok);
+    if (!bs.ok()) return bs;
+  }
+  // 4. restore
+  for (size_t k = 0; k < mine.size(); ++k) {
+    if (!saved[k]) continue;
+    const int d = slots[mine[k]];
+    const int r = ctx->slot_rank[d];
+    cudaSetDevice(ctx->ranks[r].ordinal);
+    cudaMemcpy(ctx->SlotPtr(r, d), saved[k], kSelfCheckBytes, cudaMemcpyDeviceToDevice);
+    cudaFree(saved[k]);
+  }
+  cudaGetLastError();
+  if (!all_ok) return absl::InternalError("NVLS self-check failed (multicast sums wrong or not runnable)");
+  return absl::OkStatus();
+}
+
+// Barriers of the self-check: one process sees every member's verdict
+// directly; one process per GPU all-gathers the verdicts (all ranks take
+// part, members or not, like the other setup exchanges).
+absl::Status LocalBarrier(Context*, int32_t ok, bool* all_ok) {
+  *all_ok = ok != 0;
+  return absl::OkStatus();
+}
+
+absl::Status ExchangeBarrier(Context* ctx, int32_t ok, bool* all_ok) {
+  std::vector<char> all;
+  absl::Status s = Exchange(ctx, &ok, sizeof(ok), &all);
+  if (!s.ok()) return s;
+  *all_ok = true;
+  for (int r = 0; r < ctx->world; ++r) {
+    int32_t v;
+    std::memcpy(&v, all.data() + r * sizeof(int32_t), sizeof(v));
+    *all_ok = *all_ok && v != 0;
+  }
+  return absl::OkStatus();
+}
+
 struct McShare {
   int32_t pid;
   int32_t fd;
@@ -602,6 +716,10 @@ absl::Status EnsureMulticast(Context* ctx, const std::vector<int>& slots, int* i
       std::memcpy(&v, all.data() + r * sizeof(int32_t), sizeof(v));
       if (!v) return s.ok() ? absl::InternalError(absl::StrFormat("rank %d failed to bind multicast", r)) : s;
     }
+  }
+  {
+    absl::Status chk = NvlsSelfCheck(ctx, mc.get(), slots, ctx->self_rank < 0 ? &LocalBarrier : &ExchangeBarrier);
+    if (!chk.ok()) return chk;
   }
   guard.armed = false;  // success: the context owns the group (DestroyContext releases it)
   *index = static_cast<int>(ctx->mc_index.size());

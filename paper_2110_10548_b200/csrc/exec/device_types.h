@@ -43,6 +43,9 @@ constexpr uint16_t kModeLL = 2;
 // null = local source, no wait).
 constexpr uint16_t kModeFlagSend = 3;
 constexpr uint16_t kModeFlagRecv = 4;
+// NVLS Reduce: ptrs[ptr_begin] is a multicast base; multimem.ld_reduce of
+// the task's range is stored (unicast) to the ndst destinations that follow.
+constexpr uint16_t kModeNvlsReduce = 5;
 
 // Everything one rank's kernel for one step needs (passed by value).
 struct StepArgs {
@@ -90,6 +93,8 @@ constexpr uint32_t kLLPieceBytes = 32u << 10;
 constexpr uint32_t kFlagChunk = 256u << 10;  // measured: 64 KiB -3 %, 1 MiB -3 % at K=2
 
 cudaError_t LaunchStep(const StepArgs& args, int grid, int block, int unroll, cudaStream_t stream);
+// f32 multimem.ld_reduce + multimem.st over [lo, hi) of a multicast VA.
+cudaError_t LaunchNvlsSelfCheck(char* mc, uint64_t lo, uint64_t hi, cudaStream_t stream);
 
 }  // namespace rs
 

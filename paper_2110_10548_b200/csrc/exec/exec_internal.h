@@ -66,6 +66,7 @@ typedef int (*ExchangeFn)(const void* send, size_t bytes, void* recv, void* user
 
 // A pointer-table entry: slot `slot`'s buffer (region -1) or its scratch
 // region `region`.
+enum { kReducePull = 0, kReducePush = 1, kReduceNvls = 2, kReduceNvlsRoot = 3 };
 constexpr int kMcRegion = -2;  // Ref{mc group index, kMcRegion}: a multicast base
 // Ref{source slot, kLLRegion, receiver, sender, off}: packets of the source
 // slot's data in the receiver rank's LL area, sender's block, parity-0
@@ -124,6 +125,15 @@ class Context {
   // (not measured: no 8-GPU box this round).
   uint64_t nvls_min_bytes = ~0ull;
   uint64_t nvls_min_bytes_n8 = 16ull << 20;
+  // Reduce over >= 3 GPUs (semantics.cc:292-299; the root is group[0]):
+  //   kReducePull  non-roots own slices, pull every member's copy, sum in
+  //                group order, store to the root (bit-exact; default)
+  //   kReducePush  same owners, the members land their copies in the owners'
+  //                scratch behind chunk flags (stores only; bit-exact)
+  //   kReduceNvls  every member owns a slice: multimem.ld_reduce through the
+  //                switch, unicast store to the root (f32/bf16, tolerance)
+  //   kReduceNvlsRoot  the root issues multimem.ld_reduce for all of R
+  int reduce_mode = 0;
   // One-shot (LL) steps: when every cross-GPU group of a step has its members
   // on distinct GPUs and each GPU sends any peer at most ll_max_bytes (and
   // at most 3 * ll_max_bytes in total), the

@@ -44,7 +44,8 @@ struct ProtoTask {
   Range range;
   std::vector<Ref> src;  // summation order
   std::vector<Ref> dst;
-  int mc = -1;  // >= 0: NVLS AllReduce through multicast group mc (vector body)
+  int mc = -1;  // >= 0: NVLS through multicast group mc (vector body)
+  bool mc_reduce = false;  // NVLS Reduce: ld_reduce, unicast store to dst (else AllReduce)
   // Push variant (one launch, chunk flags): a landing task (flag_send >= 0)
   // copies its vector body into the owner's memory chunk by chunk and raises
   // flag block `flag_send` per chunk; a reducing task waits for src_flag[i]
@@ -424,14 +425,37 @@ struct Compiler {
         // (Tried for n >= 3: every member owning a slice, root included — no
         // faster; push — slower; owners summing into their scratch behind
         // chunk flags with the root pulling the results — slower.)
+        const std::vector<Ref> root{Buf(g[0])};
+        int mc = -1;
+        const int mode = n >= 3 ? ctx->reduce_mode : kReducePull;
+        if ((mode == kReduceNvls || mode == kReduceNvlsRoot) && NvlsEligible(g, TotalBytes(ranges)) &&
+            !EnsureMulticast(ctx, g, &mc).ok()) {
+          ctx->nvls = false;  // consistent P2P fallback on every rank (see AllReduce)
+          mc = -1;
+        }
+        if (mc >= 0) {
+          std::vector<Ref> all;
+          for (int m : g) all.push_back(Buf(m));
+          const int owners_n = mode == kReduceNvlsRoot ? 1 : n;
+          const std::vector<std::vector<Range>> parts = SplitEven(ranges, owners_n);
+          for (int p = 0; p < owners_n; ++p) {
+            for (const Range& r : parts[p]) {
+              ProtoTask t{g[p], r, all, root, mc};
+              t.mc_reduce = true;
+              out.b.push_back(std::move(t));
+            }
+          }
+          for (int r : rows) Vid(g[0], r) = next_id++;
+          break;
+        }
         std::vector<int> owners;
         if (n == 2) {
           owners.push_back(0);
         } else {
           for (int i = 1; i < n; ++i) owners.push_back(i);
         }
-        Sums(out, g, owners, SplitEven(ranges, static_cast<int>(owners.size())), /*push=*/false,
-             [&](size_t) { return std::vector<Ref>{Buf(g[0])}; });
+        Sums(out, g, owners, SplitEven(ranges, static_cast<int>(owners.size())),
+             mode == kReducePush && PushSums(g, TotalBytes(ranges)), [&](size_t) { return root; });
         for (int r : rows) Vid(g[0], r) = next_id++;
         break;
       }
@@ -457,6 +481,25 @@ struct Compiler {
 void AddTraffic(std::vector<RankStep>& per_rank, const Context& ctx, const ProtoTask& t) {
   const double b = static_cast<double>(t.range.hi - t.range.lo);
   const int o = ctx.slot_rank[t.owner];
+  if (t.mc >= 0 && t.mc_reduce) {
+    // Switch reads every member's copy (tx b each) and returns the sum to the
+    // owner (rx b); the owner stores it to the root (unicast).
+    for (const Ref& x : t.src) {
+      RankStep& m = per_rank[ctx.slot_rank[x.slot]];
+      m.tx_bytes += b;
+      m.hbm_bytes += b;
+    }
+    per_rank[o].rx_bytes += b;
+    for (const Ref& y : t.dst) {
+      const int ry = ctx.slot_rank[y.slot];
+      per_rank[ry].hbm_bytes += b;
+      if (ry != o) {
+        per_rank[o].tx_bytes += b;
+        per_rank[ry].rx_bytes += b;
+      }
+    }
+    return;
+  }
   if (t.mc >= 0) {
     // Switch reads every member's copy (tx b each), returns the sum to the
     // owner (rx b); the multicast store leaves the owner (tx b) and lands in
@@ -605,11 +648,13 @@ void Lay(RankStep& rs, const ProtoTask& t, uint32_t piece_bytes, uint64_t flag_c
     task.ptr_begin = static_cast<uint32_t>(rs.ptr_refs.size());
     task.vec = vec ? 1u : 0u;
     if (vec && t.mc >= 0) {
-      // NVLS body: one multicast base pointer (unaligned edges stay ordered P2P sums).
-      task.mode = kModeNvlsAllReduce;
+      // NVLS body: one multicast base pointer (unaligned edges stay ordered
+      // P2P sums); a Reduce body also lists its unicast destinations.
+      task.mode = t.mc_reduce ? kModeNvlsReduce : kModeNvlsAllReduce;
       task.nsrc = 1;
-      task.ndst = 0;
+      task.ndst = t.mc_reduce ? static_cast<uint16_t>(t.dst.size()) : 0;
       rs.ptr_refs.push_back(Ref{t.mc, kMcRegion});
+      if (t.mc_reduce) rs.ptr_refs.insert(rs.ptr_refs.end(), t.dst.begin(), t.dst.end());
       rs.npieces += static_cast<uint32_t>((hi - lo + piece_bytes - 1) / piece_bytes);
       rs.tasks.push_back(task);
       return;

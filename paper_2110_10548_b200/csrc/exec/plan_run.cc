@@ -77,7 +77,7 @@ void BuildLaunches(Plan* plan) {
       a.step = static_cast<uint32_t>(ph);
       a.num_steps = static_cast<uint32_t>(P);
       for (const Task& t : rsx.tasks) {
-        a.has_nvls |= t.mode == kModeNvlsAllReduce ? 1u : 0u;
+        a.has_nvls |= (t.mode == kModeNvlsAllReduce || t.mode == kModeNvlsReduce) ? 1u : 0u;
         a.has_ll |= t.mode == kModeLL ? 1u : 0u;
       }
       const int resident = plan->ctas_per_sm * rank.sm_count;
@@ -189,13 +189,17 @@ std::string DescribePlan(const Plan& plan) {
                            {"dst_region", dst_region}, {"sends", sends}});
           continue;
         }
-        if (t.mode == kModeNvlsAllReduce) {
+        if (t.mode == kModeNvlsAllReduce || t.mode == kModeNvlsReduce) {
           const McGroup* mc = plan.ctx->mc_index[r.ptr_refs[t.ptr_begin].slot];
-          std::vector<int> none;
+          std::vector<int> mdst = mc->slots;
+          if (t.mode == kModeNvlsReduce) {
+            mdst.clear();
+            for (int i = 0; i < t.ndst; ++i) mdst.push_back(r.ptr_refs[t.ptr_begin + 1 + i].slot);
+          }
           tasks.push_back({{"lo", t.lo}, {"hi", t.hi}, {"vec", t.vec}, {"mode", t.mode},
-                           {"piece_begin", t.piece_begin}, {"src", mc->slots}, {"dst", mc->slots},
+                           {"piece_begin", t.piece_begin}, {"src", mc->slots}, {"dst", mdst},
                            {"src_region", std::vector<int>(mc->slots.size(), -1)},
-                           {"dst_region", std::vector<int>(mc->slots.size(), -1)}});
+                           {"dst_region", std::vector<int>(mdst.size(), -1)}});
           continue;
         }
         tasks.push_back({{"lo", t.lo}, {"hi", t.hi}, {"vec", t.vec}, {"mode", t.mode}, {"piece_begin", t.piece_begin},

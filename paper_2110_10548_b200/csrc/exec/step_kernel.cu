@@ -281,6 +281,42 @@ __device__ __forceinline__ void NvlsChunk(const Task& t, void* const* ptrs, uint
   }
 }
 
+// NVLS Reduce chunk: the switch sums the group's copies of the range and the
+// owner stores the result to its destinations (the root) with ordinary
+// stores. f32 / bf16 only.
+template <int DT, int kUnroll>
+__device__ __forceinline__ void NvlsReduceChunk(const Task& t, void* const* ptrs, uint64_t begin,
+                                                uint64_t end) {
+  const char* mc = static_cast<const char*>(ptrs[t.ptr_begin]);
+  void* const* dst = ptrs + t.ptr_begin + 1;
+  uint4 v[kUnroll];
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {
+    v[u] = make_uint4(0, 0, 0, 0);
+    const uint64_t off = begin + (static_cast<uint64_t>(u) * blockDim.x + threadIdx.x) * 16u;
+    if (off >= end) continue;
+    if constexpr (DT == RS_BF16) {
+      asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                   : "l"(mc + off)
+                   : "memory");
+    } else {
+      asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                   : "l"(mc + off)
+                   : "memory");
+    }
+  }
+  for (int j = 0; j < t.ndst; ++j) {
+    char* d = static_cast<char*>(dst[j]);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint64_t off = begin + (static_cast<uint64_t>(u) * blockDim.x + threadIdx.x) * 16u;
+      if (off < end) Store(d + off, v[u]);
+    }
+  }
+}
+
 __device__ __forceinline__ void FenceProxyAlias() { asm volatile("fence.proxy.alias;" ::: "memory"); }
 
 // A scalar task (< 16 bytes): one element per thread.
@@ -677,9 +713,16 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
       const uint64_t end = min(t.hi, begin + a.piece_bytes);
       const uint64_t chunk = static_cast<uint64_t>(blockDim.x) * kUnroll * 16u;
       if constexpr (DT != RS_I32) {
-        if (t.mode == kModeNvlsAllReduce) {
-          for (uint64_t c = begin; c < end; c += chunk) NvlsChunk<DT, kUnroll>(t, a.ptrs, c, min(end, c + chunk));
-          continue;
+        if constexpr (!kNc) {  // multicast objects only exist across GPUs
+          if (t.mode == kModeNvlsAllReduce) {
+            for (uint64_t c = begin; c < end; c += chunk) NvlsChunk<DT, kUnroll>(t, a.ptrs, c, min(end, c + chunk));
+            continue;
+          }
+          if (t.mode == kModeNvlsReduce) {
+            for (uint64_t c = begin; c < end; c += chunk)
+              NvlsReduceChunk<DT, kUnroll>(t, a.ptrs, c, min(end, c + chunk));
+            continue;
+          }
         }
       }
       for (uint64_t c = begin; c < end; c += chunk) VectorChunk<DT, kUnroll, kNc>(t, a.ptrs, c, min(end, c + chunk));
@@ -755,7 +798,31 @@ cudaError_t Launch(const StepArgs& a, int grid, int block, cudaStream_t stream) 
   return cudaGetLastError();
 }
 
+// NVLS self-check: f32 AllReduce of [lo, hi) through the multicast address
+// (the same instructions as the bf16/f32 NVLS tasks) — see EnsureMulticast.
+__global__ void NvlsSelfCheckKernel(char* mc, uint64_t lo, uint64_t hi) {
+  FenceProxyAlias();
+  for (uint64_t off = lo + (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 16u; off < hi;
+       off += static_cast<uint64_t>(gridDim.x) * blockDim.x * 16u) {
+    uint4 v;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(mc + off)
+                 : "memory");
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc + off), "r"(v.x),
+                 "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+  }
+  FenceProxyAlias();
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+
 }  // namespace
+
+cudaError_t LaunchNvlsSelfCheck(char* mc, uint64_t lo, uint64_t hi, cudaStream_t stream) {
+  NvlsSelfCheckKernel<<<8, 256, 0, stream>>>(mc, lo, hi);
+  return cudaGetLastError();
+}
 
 int MaxResidentCtas(int dtype, int threads, int unroll) {
   return unroll == 8 ? Occupancy<8>(dtype, threads) : Occupancy<4>(dtype, threads);

@@ -26,10 +26,13 @@ ROOT = os.path.dirname(HERE)
 
 MODE_SUM, MODE_NVLS, MODE_LL, MODE_FLAG_SEND, MODE_FLAG_RECV = 0, 1, 2, 3, 4
 VARIANTS = {
-    # name: (ll_max_bytes, push_min_bytes)
-    "ll": (256 << 10, -1),
-    "pull": (0, -1),
-    "push": (0, 0),
+    # name: context options
+    "ll": {"ll_max_bytes": 256 << 10, "push_min_bytes": -1, "reduce_mode": 0},
+    "pull": {"ll_max_bytes": 0, "push_min_bytes": -1, "reduce_mode": 0},
+    "push": {"ll_max_bytes": 0, "push_min_bytes": 0, "reduce_mode": 0},
+    # Reduce over >= 3 ranks by push (stores only, chunk flags) — the other
+    # ops as in "push"
+    "reduce_push": {"ll_max_bytes": 0, "push_min_bytes": 0, "reduce_mode": 1},
 }
 ONE_SLOT_SET = {2: "k2_flat", 4: "k4_sock", 8: "k8_sock"}
 
@@ -53,6 +56,13 @@ def _variant_used(name, desc, rank):
         return all(desc["phase_ll"])
     if name == "push":
         return MODE_FLAG_SEND in modes or MODE_FLAG_RECV in modes
+    if name == "reduce_push":
+        for st, (op, groups) in zip(desc["steps"], desc["program_steps"]):
+            if op != 3 or max(len(g) for g in groups) < 3:
+                continue
+            if any(t["mode"] in (MODE_FLAG_SEND, MODE_FLAG_RECV) for t in st["ranks"][rank]["tasks"]):
+                return True
+        return False
     return remote_pull and not (modes & {MODE_LL, MODE_FLAG_SEND, MODE_FLAG_RECV})
 
 
@@ -83,9 +93,8 @@ def worker(rank, world, port, result_dir, device_of_rank, cases):
             K, progs = golden_programs(case["set"])
             assert K == case["K"], (K, case)
             ctx = context(K)
-            ll, push = VARIANTS[case["variant"]]
-            ctx.set_option("ll_max_bytes", ll)
-            ctx.set_option("push_min_bytes", push)
+            for key, value in VARIANTS[case["variant"]].items():
+                ctx.set_option(key, value)
             N, dt = case["N"], case["dtype"]
             es = 2 if dt == numeric.BF16 else 4
             inputs = numeric.synthetic_inputs(K, N, dt)
@@ -94,6 +103,7 @@ def worker(rank, world, port, result_dir, device_of_rank, cases):
                     ctx.write(d, inputs[d])
                 plan = ctx.compile(prog, N, dt)
                 desc = plan.describe()
+                desc["program_steps"] = prog.steps
                 key = f"{case['variant']}"
                 used[key] = used.get(key, 0) + (1 if _variant_used(case["variant"], desc, rank) else 0)
                 torch.cuda.synchronize()
@@ -151,6 +161,9 @@ def default_cases(world):
         for N, dt in sizes:
             cases.append({"set": one, "K": world, "N": N, "dtype": dt, "variant": variant,
                           "stride": {2: 1, 4: 5, 8: 25}[world], "runs": 2, "graph": N % 2 == 1})
+    for N, dt in [(4097, numeric.F32), ((1 << 17) + 5, numeric.BF16), (30001, numeric.I32)]:
+        cases.append({"set": one if world > 2 else "k4_sock", "K": max(world, 4), "N": N, "dtype": dt,
+                      "variant": "reduce_push", "stride": 7, "runs": 2, "graph": dt == numeric.BF16})
     if world in (2, 4):
         for variant in ("ll", "pull", "push"):
             cases.append({"set": "cfg2_r01", "K": 8, "N": 3001, "dtype": numeric.BF16, "variant": variant,

@@ -8,6 +8,7 @@ variant is forced and checked to have run:
   pull  owners load peer sources, sum, store to peer destinations
   push  landing tasks copy into the owners' scratch behind chunk flags,
         reducing tasks wait per chunk (kModeFlagSend / kModeFlagRecv)
+  reduce_push  Reduce over >= 3 ranks by the push variant (reduce_mode 1)
 
 on every dtype, ragged sizes, CUDA-graph replays, and (world 2/4) config-2 /
 config-3 programs with several slots per rank — bit-exact against the C
@@ -32,5 +33,5 @@ def test_cross_rank_variants_on_one_gpu(tmp_path, world):
     for r, res in enumerate(results):
         assert res["ok"], f"rank {r}:\n{res['msg']}"
     used = results[0]["used"]
-    for variant in ("ll", "pull", "push"):
+    for variant in ("ll", "pull", "push", "reduce_push"):
         assert used.get(variant, 0) > 0, f"variant {variant} never ran: {used}"

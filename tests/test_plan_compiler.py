@@ -427,3 +427,52 @@ def test_copies_push_only_when_balanced():
     modes = lambda d, s: {t["mode"] for rk in d["steps"][s]["ranks"] for t in rk["tasks"]}  # noqa: E731
     assert 3 in modes(d1, 1)
     assert modes(d2, 1) <= {0}
+
+
+@pytest.mark.parametrize("mode", [1, 2, 3])
+@pytest.mark.parametrize("mapping", ["one_per_gpu", "four_gpus"])
+def test_reduce_modes_bit_exact_and_shaped(mode, mapping):
+    """Reduce over >= 3 GPUs (semantics.cc:292-299): push (mode 1, store-only
+    landing behind chunk flags) and NVLS (mode 2: every member owns a slice;
+    mode 3: the root owns all) — hazard-free plans whose ordered-sum
+    simulation equals the oracle; NVLS tasks only where a group has one slot
+    per GPU and the data is floating point."""
+    K, progs = golden_programs("cfg2_r01")
+    slot_rank, world = MAPPINGS[mapping](K)
+    ctx = executor.Context.virtual(K, slot_rank, world)
+    ctx.set_option("ll_max_bytes", 0)
+    ctx.set_option("push_min_bytes", 0)
+    ctx.set_option("reduce_mode", mode)
+    if mode >= 2:
+        ctx.set_option("nvls", 1)
+        ctx.set_option("nvls_min_bytes", 0)
+    reduce_progs = [p for _, _, p, _ in progs if any(op == 3 for op, _ in p.steps)]
+    seen = 0
+    for prog in reduce_progs[::7]:
+        for dtype in (numeric.BF16, numeric.I32):
+            desc = ctx.compile(prog, 4099, dtype).describe()
+            for st, (op, groups) in zip(desc["steps"], prog.steps):
+                if op != 3:
+                    continue
+                for rk in st["ranks"]:
+                    for t in rk["tasks"]:
+                        if t.get("mode") == 5:
+                            seen += 1
+                            assert mode >= 2 and dtype != numeric.I32
+                            assert len(t["src"]) >= 4 and len(t["dst"]) == 1 and t["dst"][0] == t["src"][0]
+                        if mode == 1 and t.get("mode") in (3, 4):
+                            seen += 1
+            inputs = numeric.synthetic_inputs(K, 4099, dtype)
+            want = [x.copy() for x in inputs]
+            numeric.execute(prog, K, want, dtype, nthreads=1)
+            got = [x.copy() for x in inputs]
+            simulate_plan(desc, got, dtype)
+            assert all(np.array_equal(a.view(np.uint8), b.view(np.uint8)) for a, b in zip(got, want)), prog.text
+    if mapping == "one_per_gpu" or mode == 1:
+        assert seen > 0
+
+
+def test_reduce_mode_option_validated():
+    ctx = executor.Context.virtual(4, [0, 1, 2, 3], 4)
+    with pytest.raises(ExecError):
+        ctx.set_option("reduce_mode", 7)

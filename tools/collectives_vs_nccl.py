@@ -19,7 +19,13 @@ def main():
     ap.add_argument("--step", type=int, default=8)
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--ops", default="AllReduce,ReduceScatter,Reduce")
+    ap.add_argument("--reduce-modes", default="0",
+                    help="comma list of executor Reduce variants to time (0 pull, 1 push, 2 NVLS, 3 NVLS root)")
+    ap.add_argument("--nvls", action="store_true", help="multicast-capable heaps (RS_NVLS=1; needed by modes 2/3)")
     args = ap.parse_args()
+    if args.nvls:
+        os.environ["RS_NVLS"] = "1"
     import torch
     import torch.distributed as dist
     from paper_2110_10548_b200 import executor
@@ -30,9 +36,14 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.current_stream(dev)
     ctx = executor.Context.from_process_group(world, list(range(world)), args.max_bytes)
+    if args.nvls:
+        ctx.set_option("nvls_min_bytes", 0)
     g = list(range(world))
+    ops = args.ops.split(",")
+    modes = [int(m) for m in args.reduce_modes.split(",")]
     progs = {"AllReduce": LoweredProgram(steps=[(0, [g])]), "ReduceScatter": LoweredProgram(steps=[(1, [g])]),
              "Reduce": LoweredProgram(steps=[(3, [g])])}
+    progs = {k: v for k, v in progs.items() if k in ops}
 
     def timed(fn):
         for _ in range(3):
@@ -72,11 +83,17 @@ def main():
                 "Reduce": lambda: dist.reduce(x, dst=0)}
         row = {"bytes": size}
         for name, prog in progs.items():
-            plan = ctx.compile(prog, elems, "bf16")
-            ours = timed(plan.run)
-            plan.close()
             theirs = timed(nccl[name])
-            row[name] = {"ours_us": round(ours, 2), "nccl_us": round(theirs, 2), "speedup": round(theirs / ours, 3)}
+            for mode in (modes if name == "Reduce" else [None]):
+                if mode is not None:
+                    ctx.set_option("reduce_mode", mode)
+                plan = ctx.compile(prog, elems, "bf16")
+                ours = timed(plan.run)
+                used = sorted({t["mode"] for st in plan.describe()["steps"] for rk in st["ranks"] for t in rk["tasks"]})
+                plan.close()
+                key = name if mode is None else f"{name}[mode {mode}]"
+                row[key] = {"ours_us": round(ours, 2), "nccl_us": round(theirs, 2), "speedup": round(theirs / ours, 3),
+                            "task_modes": used}
         rows.append(row)
         if rank == 0:
             print(json.dumps(row), flush=True)
