@@ -260,11 +260,13 @@ int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value) {
     ctx->impl->nvls_min_bytes_n8 = ctx->impl->nvls_min_bytes;
   } else if (k == "ll_max_bytes") {
     ctx->impl->ll_max_bytes = value < 0 ? 0 : static_cast<uint64_t>(value);
+  } else if (k == "push_wave_bytes") {
+    ctx->impl->push_wave_bytes = value <= 0 ? 0 : (static_cast<uint64_t>(value) & ~15ull);
   } else if (k == "reduce_mode") {
     if (value < rs::kReducePull || value > rs::kReduceNvlsRoot) return Bad("reduce_mode must be 0 (pull), 1 (push), 2 (nvls) or 3 (nvls root)");
     ctx->impl->reduce_mode = static_cast<int>(value);
   } else {
-    return Bad("unknown option (push_min_bytes | barrier_timeout_ms | nvls | nvls_min_group | nvls_min_bytes | ll_max_bytes | reduce_mode)");
+    return Bad("unknown option (push_min_bytes | barrier_timeout_ms | nvls | nvls_min_group | nvls_min_bytes | ll_max_bytes | reduce_mode | push_wave_bytes)");
   }
   return RS_OK;
 }
@@ -303,8 +305,12 @@ int rs_plan_set_option(rs_plan* plan, const char* key, long long value) {
     return rs_plan_set_launch(plan, plan->impl->max_ctas, static_cast<int>(value));
   } else if (k == "max_ctas") {
     plan->impl->max_ctas = value < 0 ? 0 : static_cast<int>(value);
+  } else if (k == "wide_loads") {
+    plan->impl->wide_loads = value != 0;
+  } else if (k == "dynamic_pieces") {
+    plan->impl->dynamic_pieces = value != 0;
   } else {
-    return Bad("unknown option (unroll | threads | max_ctas)");
+    return Bad("unknown option (unroll | threads | max_ctas | wide_loads | dynamic_pieces)");
   }
   plan->impl->ctas_per_sm = 0;
   return RS_OK;

@@ -151,6 +151,9 @@ void ReadTimeoutEnv(Context* ctx) {
     ctx->push_min_bytes = std::strtoull(env, nullptr, 10);
   }
   if (const char* env = std::getenv("RS_PUSH_MAX_GPUS")) ctx->push_max_gpus = std::atoi(env);
+  if (const char* env = std::getenv("RS_PUSH_WAVE_BYTES")) {
+    ctx->push_wave_bytes = std::strtoull(env, nullptr, 10) & ~15ull;
+  }
   if (const char* env = std::getenv("RS_REDUCE_MODE")) {
     const int m = std::atoi(env);
     if (m >= kReducePull && m <= kReduceNvlsRoot) ctx->reduce_mode = m;

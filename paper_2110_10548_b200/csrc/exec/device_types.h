@@ -56,6 +56,8 @@ struct StepArgs {
   uint32_t piece_bytes;         // bytes per vector piece = threads * unroll * 16
   int32_t dtype;
   unsigned int* arrive_counter;  // this rank's CTA-arrival counter
+  unsigned int* piece_counter;   // [0] next piece, [1] CTAs done (dynamic push phases)
+  uint32_t dynamic;              // pieces handed out by piece_counter (push phases)
   int* error_flag;               // set to 1 on a barrier timeout
   const uint64_t* inbox;         // this rank's flags, inbox[q] = last epoch of rank q
   uint64_t* signal_ptrs[RS_MAX_RANKS];  // &inbox_of_rank_q[my_rank], every other rank q
@@ -79,7 +81,9 @@ struct StepArgs {
   uint64_t ll_parity_stride;  // bytes between the two parity regions of an LL block
   uint32_t flag_chunk;        // push-variant chunk (bytes per flag)
   uint32_t local_only;        // single-rank context: sources are read-only for the launch (.nc loads)
+  uint32_t wide_loads;        // cross-GPU pull sums load every source before adding (VectorChunkWide)
   uint32_t solo;              // profiling builds only (RS_PROFILING_AIDS): skip every cross-GPU wait
+  uint64_t* trace;            // profiling builds only: %globaltimer stamps per piece (RS_TRACE_PTR)
 };
 
 // Vector work is cut into pieces of kPieceBytes; a CTA walks a piece in

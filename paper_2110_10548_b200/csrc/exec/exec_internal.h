@@ -20,6 +20,7 @@ namespace rs {
 // Heap layout of every rank (one cudaMalloc per rank, shared by IPC):
 //   [0, 64)        inbox: uint64 epoch per peer rank (written remotely)
 //   [256, 260)     CTA-arrival counter
+//   [320, 328)     piece queue: next piece, CTAs done (push phases)
 //   [512, 516)     barrier-timeout error flag
 //   [768, 776)     run base epoch (device resident, starts at 1)
 //   [2 MiB, ...)   per hosted slot: its buffer, then `scratch_regions`
@@ -33,6 +34,7 @@ namespace rs {
 //                  slot buffer and scratch region
 constexpr size_t kInboxOffset = 0;
 constexpr size_t kCounterOffset = 256;
+constexpr size_t kPieceCounterOffset = 320;  // [320, 328): piece queue of push phases
 constexpr size_t kErrorOffset = 512;
 constexpr size_t kEpochOffset = 768;
 constexpr size_t kDataOffset = 2u << 20;  // multicast-bind granularity
@@ -111,6 +113,10 @@ class Context {
   // to 1 GiB vs pull 596-646 and NVLS 588-681 (profiles/r01_sweep_k4_push.txt).
   uint64_t push_min_bytes = 32ull << 20;
   int push_max_gpus = RS_MAX_RANKS;  // RS_PUSH_MAX_GPUS
+  // Push waves (option "push_wave_bytes", env RS_PUSH_WAVE_BYTES; 0 = one
+  // wave): parts are landed and reduced wave by wave so result traffic
+  // overlaps landing traffic.
+  uint64_t push_wave_bytes = 0;
   // NVLS: AllReduce groups of >= nvls_min_group slots on distinct GPUs use
   // multimem.ld_reduce + multimem.st through the NVSwitch (needs a VMM heap,
   // RS_NVLS=1 at creation; sums then follow the switch's order: f32/bf16
@@ -196,6 +202,8 @@ class Plan {
   int unroll = 4;      // 4 or 8 vectors in flight per thread per source
   int max_ctas = 0;    // 0 = resident capacity
   int ctas_per_sm = 0;  // resident capacity for (dtype, threads, unroll); 0 = recompute
+  bool dynamic_pieces = true;  // push phases take pieces from an atomic queue (option / env RS_DYNAMIC_PIECES)
+  bool wide_loads = true;  // cross-GPU pull sums: all sources in flight (option "wide_loads", env RS_WIDE_LOADS)
   // Launch phases, one per program step (every variant — pull, push with
   // chunk flags, one-shot, NVLS — runs its step in a single launch).
   std::vector<std::vector<RankStep>> phases;  // [phase][rank]

@@ -21,6 +21,7 @@
 // 4. Computes each rank's entry-barrier set per phase (ranks whose memory it
 //    touches and their previous-phase writers) and the run's tail barrier.
 #include <algorithm>
+#include <limits>
 #include <map>
 #include <memory>
 #include <cstdlib>
@@ -54,6 +55,7 @@ struct ProtoTask {
   int flag_send = -1;
   std::vector<int> src_flag;
   std::vector<Ref> edge_src, edge_dst;
+  int wave = 0;  // push variant: pipeline wave (launch order: wave, then landing before reducing)
 };
 
 Ref Buf(int slot) { return Ref{slot, -1}; }
@@ -163,6 +165,24 @@ struct Compiler {
   }
   uint64_t& Vid(int d, int r) { return vid[static_cast<size_t>(d) * K + r]; }
 
+  // Push variant: a part is cut into waves of ctx->push_wave_bytes (16-byte
+  // aligned cuts); landing and reducing tasks of wave w are laid out before
+  // those of wave w+1, so owners reduce (and results leave) while later
+  // waves still land — landing and result traffic overlap on every link.
+  std::vector<Range> Waves(const Range& r) const {
+    const uint64_t w = ctx->push_wave_bytes;
+    if (w == 0 || r.hi - r.lo <= w) return {r};
+    std::vector<Range> out;
+    const uint64_t a = (r.lo + 15) & ~uint64_t{15};
+    uint64_t lo = r.lo;
+    for (uint64_t cut = a + w; cut < r.hi; cut += w) {
+      out.push_back(Range{lo, cut});
+      lo = cut;
+    }
+    out.push_back(Range{lo, r.hi});
+    return out;
+  }
+
   bool SpansRanks(const std::vector<int>& g) const {
     for (int d : g)
       if (ctx->slot_rank[d] != ctx->slot_rank[g[0]]) return true;
@@ -208,23 +228,29 @@ struct Compiler {
       const int rp = ctx->slot_rank[g[p]];
       std::vector<Ref> pull_src;
       for (int m : g) pull_src.push_back(Buf(m));
-      for (const Range& r : parts[j]) {
-        ProtoTask b{g[p], r, {}, dst_of(j)};
-        for (int i = 0; i < n; ++i) {
-          if (i == p || ctx->slot_rank[g[i]] == rp) {
-            b.src.push_back(Buf(g[i]));
-            b.src_flag.push_back(-1);
-            continue;
+      int wave = 0;
+      for (const Range& part : parts[j]) {
+        for (const Range& r : Waves(part)) {
+          ProtoTask b{g[p], r, {}, dst_of(j)};
+          b.wave = wave;
+          for (int i = 0; i < n; ++i) {
+            if (i == p || ctx->slot_rank[g[i]] == rp) {
+              b.src.push_back(Buf(g[i]));
+              b.src_flag.push_back(-1);
+              continue;
+            }
+            ProtoTask a{g[i], r, {Buf(g[i])}, {Ref{g[p], i}}};
+            a.flag_send = next_flag++;
+            a.wave = wave;
+            b.src.push_back(Ref{g[p], i});
+            b.src_flag.push_back(a.flag_send);
+            out.a.push_back(std::move(a));
           }
-          ProtoTask a{g[i], r, {Buf(g[i])}, {Ref{g[p], i}}};
-          a.flag_send = next_flag++;
-          b.src.push_back(Ref{g[p], i});
-          b.src_flag.push_back(a.flag_send);
-          out.a.push_back(std::move(a));
+          b.edge_src = pull_src;
+          b.edge_dst = b.dst;
+          out.b.push_back(std::move(b));
+          ++wave;
         }
-        b.edge_src = pull_src;
-        b.edge_dst = b.dst;
-        out.b.push_back(std::move(b));
       }
     }
   }
@@ -266,15 +292,20 @@ struct Compiler {
           // chunk; (B) receiver j fans each landed chunk out to the others.
           std::vector<Ref> all_dst;
           for (int m : recv) all_dst.push_back(Buf(m));
-          for (const Range& r : parts[j]) {
-            ProtoTask a{h, r, {Buf(h)}, {Buf(recv[j])}};
-            a.flag_send = next_flag++;
-            ProtoTask b{recv[j], r, {Buf(recv[j])}, others};
-            b.src_flag = {a.flag_send};
-            b.edge_src = {Buf(h)};
-            b.edge_dst = all_dst;
-            out.a.push_back(std::move(a));
-            out.b.push_back(std::move(b));
+          int wave = 0;
+          for (const Range& part : parts[j]) {
+            for (const Range& r : Waves(part)) {
+              ProtoTask a{h, r, {Buf(h)}, {Buf(recv[j])}};
+              a.flag_send = next_flag++;
+              a.wave = wave;
+              ProtoTask b{recv[j], r, {Buf(recv[j])}, others};
+              b.src_flag = {a.flag_send};
+              b.edge_src = {Buf(h)};
+              b.edge_dst = all_dst;
+              b.wave = wave++;
+              out.a.push_back(std::move(a));
+              out.b.push_back(std::move(b));
+            }
           }
         } else {
           std::vector<Ref> dst;
@@ -906,6 +937,8 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
     if (u == 4 || u == 8) plan->unroll = u;
   }
   if (const char* v = std::getenv("RS_MAX_CTAS")) plan->max_ctas = std::max(0, std::atoi(v));
+  if (const char* v = std::getenv("RS_WIDE_LOADS")) plan->wide_loads = std::atoi(v) != 0;
+  if (const char* v = std::getenv("RS_DYNAMIC_PIECES")) plan->dynamic_pieces = std::atoi(v) != 0;
 
   // 2./3. Tasks per step, laid out into one launch phase per step.
   Compiler comp(ctx, elems, es, dtype);
@@ -957,17 +990,24 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
     }
     // One launch: push landing tasks first (every CTA sends before it waits
     // for chunks), then the reducing / pull tasks.
+    // Order: per push wave, its landing tasks (each sender walking the
+    // receiving GPUs starting after itself, so at any moment the GPUs push
+    // into different peers rather than all into one), then its reducing /
+    // fan-out tasks; tasks without flags (pull) last. Every CTA meets a
+    // wave's landing pieces before that wave's reducing pieces, so the waits
+    // cannot deadlock (all CTAs of a launch are resident).
     std::vector<ProtoTask> list = std::move(tasks.a);
-    // Each sender walks the receiving GPUs starting after itself, so at any
-    // moment the GPUs push into different peers rather than all into one.
-    std::stable_sort(list.begin(), list.end(), [&](const ProtoTask& x, const ProtoTask& y) {
-      auto rot = [&](const ProtoTask& t) {
-        const int from = ctx->slot_rank[t.owner];
-        return (ctx->slot_rank[t.dst[0].slot] - from + R) % R;
-      };
-      return rot(x) < rot(y);
-    });
     list.insert(list.end(), tasks.b.begin(), tasks.b.end());
+    auto order_key = [&](const ProtoTask& t) {
+      if (t.flag_send >= 0) {
+        const int from = ctx->slot_rank[t.owner];
+        return std::make_tuple(t.wave, 0, (ctx->slot_rank[t.dst[0].slot] - from + R) % R);
+      }
+      if (!t.src_flag.empty()) return std::make_tuple(t.wave, 1, 0);
+      return std::make_tuple(std::numeric_limits<int>::max(), 2, 0);
+    };
+    std::stable_sort(list.begin(), list.end(),
+                     [&](const ProtoTask& x, const ProtoTask& y) { return order_key(x) < order_key(y); });
     plan->phases.emplace_back(R);
     plan->phase_step.push_back(s);
     plan->phase_ll.push_back(0);

@@ -69,16 +69,22 @@ void BuildLaunches(Plan* plan) {
         a.nfinal = 0;
         a.solo = 1;
       }
+      // Piece timeline (tools/trace_push.py): RS_TRACE_PTR = device address
+      // of a buffer on this rank's GPU, >= 3 * npieces + 2 * grid uint64.
+      if (const char* tp = std::getenv("RS_TRACE_PTR")) a.trace = reinterpret_cast<uint64_t*>(std::strtoull(tp, nullptr, 10));
 #endif
       a.local_only = ctx->world == 1 ? 1u : 0u;
+      a.wide_loads = plan->wide_loads ? 1u : 0u;
       a.signal_done = rsx.signal_done ? 1u : 0u;
       a.wait_lag = static_cast<uint32_t>(plan->phase_lag[ph]);
       a.epoch_base = reinterpret_cast<uint64_t*>(rank.heap + kEpochOffset);
       a.step = static_cast<uint32_t>(ph);
       a.num_steps = static_cast<uint32_t>(P);
+      a.piece_counter = reinterpret_cast<unsigned int*>(rank.heap + kPieceCounterOffset);
       for (const Task& t : rsx.tasks) {
         a.has_nvls |= (t.mode == kModeNvlsAllReduce || t.mode == kModeNvlsReduce) ? 1u : 0u;
         a.has_ll |= t.mode == kModeLL ? 1u : 0u;
+        a.dynamic |= (plan->dynamic_pieces && (t.mode == kModeFlagSend || t.mode == kModeFlagRecv)) ? 1u : 0u;
       }
       const int resident = plan->ctas_per_sm * rank.sm_count;
       int cap = plan->max_ctas > 0 ? std::min(plan->max_ctas, resident) : resident;

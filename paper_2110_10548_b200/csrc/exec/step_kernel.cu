@@ -240,6 +240,56 @@ __device__ __forceinline__ void VectorChunk(const Task& t, void* const* ptrs, ui
   }
 }
 
+// Cross-GPU pull chunk with every source's loads in flight at once: all
+// nsrc (<= kS) sources' kU vectors are loaded before the first add, so a
+// chunk costs one round trip instead of nsrc serialized ones; the sum is
+// still taken in source (group) order. Remote loads are weak ld.global.
+template <int DT, int kS, int kU>
+__device__ __forceinline__ void VectorChunkWide(const Task& t, void* const* ptrs, uint64_t begin,
+                                                uint64_t end) {
+  using Acc = typename AccOf<DT>::T;
+  uint64_t off[kU];
+  bool ok[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    off[u] = begin + (static_cast<uint64_t>(u) * blockDim.x + threadIdx.x) * 16u;
+    ok[u] = off[u] < end;
+  }
+  void* const* src = ptrs + t.ptr_begin;
+  void* const* dst = src + t.nsrc;
+  uint4 raw[kS][kU];
+#pragma unroll
+  for (int i = 0; i < kS; ++i) {
+#pragma unroll
+    for (int u = 0; u < kU; ++u) raw[i][u] = make_uint4(0, 0, 0, 0);
+    if (i < t.nsrc) {
+      const char* si = static_cast<const char*>(src[i]);
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (ok[u]) raw[i][u] = LoadStream<false>(si + off[u]);
+    }
+  }
+  Acc acc[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) acc[u].Init(raw[0][u]);
+#pragma unroll
+  for (int i = 1; i < kS; ++i) {
+    if (i < t.nsrc) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) acc[u].Add(raw[i][u]);
+    }
+  }
+  uint4 out[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) out[u] = acc[u].Pack();
+  for (int j = 0; j < t.ndst; ++j) {
+    char* d = static_cast<char*>(dst[j]);
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (ok[u]) Store(d + off[u], out[u]);
+  }
+}
+
 // NVLS AllReduce chunk: the NVSwitch sums the group's copies
 // (multimem.ld_reduce on the multicast address; bf16 accumulates in f32) and
 // multimem.st writes the result to every member. f32 / bf16 only.
@@ -629,6 +679,21 @@ __device__ __forceinline__ void LLReceive(const Task& t, void* const* ptrs, uint
   }
 }
 
+// Profiling builds only: %globaltimer stamps by thread 0 — per piece p
+// trace[3p] = start, [3p+1] = inputs ready (after flag waits), [3p+2] = end;
+// per CTA b (after the pieces) trace[3*npieces + 2b] = entry,
+// [3*npieces + 2b + 1] = entry barrier passed.
+#ifdef RS_PROFILING_AIDS
+#define RS_TRACE(idx)                                   \
+  do {                                                  \
+    if (a.trace && threadIdx.x == 0) a.trace[idx] = GlobalTimer(); \
+  } while (0)
+#else
+#define RS_TRACE(idx) \
+  do {                \
+  } while (0)
+#endif
+
 // One launch phase of one rank: entry barrier, tasks, exit.
 template <int DT, int kUnroll, bool kLL, bool kNc>
 __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
@@ -641,10 +706,12 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
   }
   // 2. Entry barrier: the ranks whose buffers this step touches (and whose
   //    previous-step writers) have finished the previous step.
+  RS_TRACE(3ull * a.npieces + 2ull * blockIdx.x);
   if (threadIdx.x < a.nwait) {
     WaitAtLeast(a.inbox + a.wait_ranks[threadIdx.x], base + a.step - a.wait_lag, a.timeout_ns, a.error_flag);
   }
   __syncthreads();
+  RS_TRACE(3ull * a.npieces + 2ull * blockIdx.x + 1);
   if (a.has_nvls) FenceProxyAlias();
 
   // 3. Pieces, grid-strided; tasks are ordered by piece_begin. One-shot
@@ -668,15 +735,16 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
     }
   }
   uint32_t cur = 0;
-  for (uint32_t p = blockIdx.x; p < a.npieces; p += gridDim.x) {
+  auto run_piece = [&](const uint32_t p) {
     while (cur + 1 < a.ntasks && a.tasks[cur + 1].piece_begin <= p) ++cur;
     const Task& t = a.tasks[cur];
     if (kLL && t.mode == kModeLL) {
       uint64_t begin, end;
       ll_range(t, p, begin, end);
       LLReceive<DT>(t, a.ptrs, begin, end, static_cast<uint32_t>(epoch), parity_off, a.timeout_ns, a.error_flag);
-      continue;
+      return;
     }
+    RS_TRACE(3ull * p);
     if (t.mode == kModeFlagSend || t.mode == kModeFlagRecv) {
       // Push variant, one flag_chunk piece: land it and raise its flag, or
       // wait for every pushed source's flag and reduce it.
@@ -695,40 +763,80 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
           WaitAtLeast(static_cast<const uint64_t*>(flags[threadIdx.x]) + k, epoch, a.timeout_ns, a.error_flag);
         }
         __syncthreads();
+        RS_TRACE(3ull * p + 1);
         for (uint64_t c = begin; c < end; c += chunk)
           VectorChunk<DT, kUnroll, kNc, true>(t, a.ptrs, c, min(end, c + chunk));
       } else {
         for (uint64_t c = begin; c < end; c += chunk)
           VectorChunk<DT, kUnroll, kNc>(t, a.ptrs, c, min(end, c + chunk));
         __syncthreads();
+        RS_TRACE(3ull * p + 1);
         if (threadIdx.x == 0) {
           FenceSys();
           StoreRelaxedSys(static_cast<uint64_t*>(flags[0]) + k, epoch);
         }
       }
-      continue;
+      RS_TRACE(3ull * p + 2);
+      return;
     }
     if (t.vec) {
       const uint64_t begin = t.lo + static_cast<uint64_t>(p - t.piece_begin) * a.piece_bytes;
       const uint64_t end = min(t.hi, begin + a.piece_bytes);
       const uint64_t chunk = static_cast<uint64_t>(blockDim.x) * kUnroll * 16u;
-      if constexpr (DT != RS_I32) {
-        if constexpr (!kNc) {  // multicast objects only exist across GPUs
-          if (t.mode == kModeNvlsAllReduce) {
-            for (uint64_t c = begin; c < end; c += chunk) NvlsChunk<DT, kUnroll>(t, a.ptrs, c, min(end, c + chunk));
-            continue;
-          }
-          if (t.mode == kModeNvlsReduce) {
-            for (uint64_t c = begin; c < end; c += chunk)
-              NvlsReduceChunk<DT, kUnroll>(t, a.ptrs, c, min(end, c + chunk));
-            continue;
-          }
+      bool done = false;
+      if constexpr (DT != RS_I32 && !kNc) {  // multicast objects only exist across GPUs
+        if (t.mode == kModeNvlsAllReduce) {
+          for (uint64_t c = begin; c < end; c += chunk) NvlsChunk<DT, kUnroll>(t, a.ptrs, c, min(end, c + chunk));
+          done = true;
+        } else if (t.mode == kModeNvlsReduce) {
+          for (uint64_t c = begin; c < end; c += chunk)
+            NvlsReduceChunk<DT, kUnroll>(t, a.ptrs, c, min(end, c + chunk));
+          done = true;
         }
       }
-      for (uint64_t c = begin; c < end; c += chunk) VectorChunk<DT, kUnroll, kNc>(t, a.ptrs, c, min(end, c + chunk));
+      if constexpr (!kNc) {
+        if (!done && a.wide_loads && t.nsrc >= 2 && t.nsrc <= 8) {
+          // cross-GPU sums: every source in flight at once (see VectorChunkWide)
+          if (t.nsrc <= 4) {
+            constexpr uint64_t kW = 2;
+            const uint64_t wchunk = static_cast<uint64_t>(blockDim.x) * kW * 16u;
+            for (uint64_t c = begin; c < end; c += wchunk)
+              VectorChunkWide<DT, 4, kW>(t, a.ptrs, c, min(end, c + wchunk));
+          } else {
+            const uint64_t wchunk = static_cast<uint64_t>(blockDim.x) * 16u;
+            for (uint64_t c = begin; c < end; c += wchunk)
+              VectorChunkWide<DT, 8, 1>(t, a.ptrs, c, min(end, c + wchunk));
+          }
+          done = true;
+        }
+      }
+      if (!done) {
+        for (uint64_t c = begin; c < end; c += chunk) VectorChunk<DT, kUnroll, kNc>(t, a.ptrs, c, min(end, c + chunk));
+      }
     } else {
       ScalarTask<DT>(t, a.ptrs);
     }
+    RS_TRACE(3ull * p + 2);
+  };
+  // Push phases (a.dynamic): pieces are handed out in launch order through
+  // an atomic counter, so a CTA takes a wave's reducing piece only after
+  // every landing piece of that wave has been taken (no CTA sits on a flag
+  // wait while landing work is left unclaimed; deadlock-free because landing
+  // pieces never wait). Other phases: static grid stride.
+  __shared__ uint32_t next_piece;
+  auto next = [&](uint32_t p) -> uint32_t {
+    if (!a.dynamic) return p + gridDim.x;
+    if (threadIdx.x == 0) next_piece = atomicAdd(a.piece_counter, 1u);
+    __syncthreads();
+    const uint32_t q = next_piece;
+    __syncthreads();
+    return q;
+  };
+  for (uint32_t p = a.dynamic ? next(0) : blockIdx.x; p < a.npieces; p = next(p)) run_piece(p);
+  if (a.dynamic && threadIdx.x == 0 && atomicAdd(a.piece_counter + 1, 1u) == gridDim.x - 1) {
+    // last CTA out: reset the queue for the next launch on this rank
+    atomicExch(a.piece_counter, 0u);
+    atomicExch(a.piece_counter + 1, 0u);
   }
 
   // 4. Exit: the last CTA to finish publishes the step's epoch to all ranks

@@ -476,3 +476,41 @@ def test_reduce_mode_option_validated():
     ctx = executor.Context.virtual(4, [0, 1, 2, 3], 4)
     with pytest.raises(ExecError):
         ctx.set_option("reduce_mode", 7)
+
+
+@pytest.mark.parametrize("mapping", ["one_per_gpu", "two_gpus", "interleaved2"])
+@pytest.mark.parametrize("reduce_mode", [0, 1])
+def test_push_waves_bit_exact_and_ordered(mapping, reduce_mode):
+    """Push waves (push_wave_bytes): parts are cut into waves whose landing
+    tasks precede their reducing tasks and every earlier wave's tasks — the
+    plan stays hazard-free and equal to the oracle; unaligned part edges
+    still pull (scalar tasks only at the true edges)."""
+    K, progs = golden_programs("cfg2_r01")
+    slot_rank, world = MAPPINGS[mapping](K)
+    ctx = executor.Context.virtual(K, slot_rank, world)
+    ctx.set_option("ll_max_bytes", 0)
+    ctx.set_option("push_min_bytes", 0)
+    ctx.set_option("push_wave_bytes", 16 << 10)
+    ctx.set_option("reduce_mode", reduce_mode)
+    N = (1 << 17) + 3
+    waves = 0
+    for _, _, prog, _ in progs[::23]:
+        desc = ctx.compile(prog, N, numeric.BF16).describe()
+        for st in desc["steps"]:
+            for rk in st["ranks"]:
+                modes = [t["mode"] for t in rk["tasks"]]
+                sends = [i for i, m in enumerate(modes) if m == 3]
+                recvs = [i for i, m in enumerate(modes) if m == 4]
+                if len(sends) > 1:
+                    waves += 1
+                # interleaved: some reducing task precedes the last landing task
+                if len(sends) > 4 and recvs:
+                    assert recvs[0] < sends[-1], modes
+                assert sum(1 for t in rk["tasks"] if not t["vec"]) <= 4 * len(rk["tasks"])
+        inputs = numeric.synthetic_inputs(K, N, numeric.BF16)
+        want = [x.copy() for x in inputs]
+        numeric.execute(prog, K, want, numeric.BF16, nthreads=1)
+        got = [x.copy() for x in inputs]
+        simulate_plan(desc, got, numeric.BF16)
+        assert all(np.array_equal(a.view(np.uint8), b.view(np.uint8)) for a, b in zip(got, want)), prog.text
+    assert waves > 0

@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--reduce-modes", default="0",
                     help="comma list of executor Reduce variants to time (0 pull, 1 push, 2 NVLS, 3 NVLS root)")
     ap.add_argument("--nvls", action="store_true", help="multicast-capable heaps (RS_NVLS=1; needed by modes 2/3)")
+    ap.add_argument("--push-min-bytes", type=int, default=None, help="context push threshold (-1 = never push)")
+    ap.add_argument("--wave-bytes", type=int, default=None, help="push waves (0 = one wave)")
     args = ap.parse_args()
     if args.nvls:
         os.environ["RS_NVLS"] = "1"
@@ -36,8 +38,10 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.current_stream(dev)
     ctx = executor.Context.from_process_group(world, list(range(world)), args.max_bytes)
-    if args.nvls:
-        ctx.set_option("nvls_min_bytes", 0)
+    if args.push_min_bytes is not None:
+        ctx.set_option("push_min_bytes", args.push_min_bytes)
+    if args.wave_bytes is not None:
+        ctx.set_option("push_wave_bytes", args.wave_bytes)
     g = list(range(world))
     ops = args.ops.split(",")
     modes = [int(m) for m in args.reduce_modes.split(",")]
@@ -87,6 +91,8 @@ def main():
             for mode in (modes if name == "Reduce" else [None]):
                 if mode is not None:
                     ctx.set_option("reduce_mode", mode)
+                if args.nvls:  # NVLS only where a Reduce mode asks for it (AllReduce stays P2P below 8 GPUs)
+                    ctx.set_option("nvls_min_bytes", 0 if mode in (2, 3) else -1)
                 plan = ctx.compile(prog, elems, "bf16")
                 ours = timed(plan.run)
                 used = sorted({t["mode"] for st in plan.describe()["steps"] for rk in st["ranks"] for t in rk["tasks"]})
