@@ -68,7 +68,7 @@ typedef int (*ExchangeFn)(const void* send, size_t bytes, void* recv, void* user
 
 // A pointer-table entry: slot `slot`'s buffer (region -1) or its scratch
 // region `region`.
-enum { kReducePull = 0, kReducePush = 1, kReduceNvls = 2, kReduceNvlsRoot = 3 };
+enum { kReduceAuto = -1, kReducePull = 0, kReducePush = 1, kReduceNvls = 2, kReduceNvlsRoot = 3 };
 constexpr int kMcRegion = -2;  // Ref{mc group index, kMcRegion}: a multicast base
 // Ref{source slot, kLLRegion, receiver, sender, off}: packets of the source
 // slot's data in the receiver rank's LL area, sender's block, parity-0
@@ -139,7 +139,14 @@ class Context {
   //   kReduceNvls  every member owns a slice: multimem.ld_reduce through the
   //                switch, unicast store to the root (f32/bf16, tolerance)
   //   kReduceNvlsRoot  the root issues multimem.ld_reduce for all of R
-  int reduce_mode = 0;
+  //   kReduceAuto  (default) pull below reduce_push_min_bytes, push with
+  //                reduce_wave_bytes waves from there. Measured at K=4 bf16
+  //                (profiles/r02_reduce_variants_k4.txt): pull 166 / 613 /
+  //                2425 us at 64 MiB / 256 MiB / 1 GiB, push with 4 MiB
+  //                waves 194 / 554 / 1942 us.
+  int reduce_mode = kReduceAuto;
+  uint64_t reduce_push_min_bytes = 128ull << 20;
+  uint64_t reduce_wave_bytes = 4ull << 20;
   // One-shot (LL) steps: when every cross-GPU group of a step has its members
   // on distinct GPUs and each GPU sends any peer at most ll_max_bytes (and
   // at most 3 * ll_max_bytes in total), the

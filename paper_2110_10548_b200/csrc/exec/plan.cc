@@ -169,8 +169,8 @@ struct Compiler {
   // aligned cuts); landing and reducing tasks of wave w are laid out before
   // those of wave w+1, so owners reduce (and results leave) while later
   // waves still land — landing and result traffic overlap on every link.
-  std::vector<Range> Waves(const Range& r) const {
-    const uint64_t w = ctx->push_wave_bytes;
+  std::vector<Range> Waves(const Range& r, uint64_t wave_bytes = ~0ull) const {
+    const uint64_t w = wave_bytes == ~0ull ? ctx->push_wave_bytes : wave_bytes;
     if (w == 0 || r.hi - r.lo <= w) return {r};
     std::vector<Range> out;
     const uint64_t a = (r.lo + 15) & ~uint64_t{15};
@@ -191,14 +191,15 @@ struct Compiler {
   // Push needs every sender to land its share in the owner's memory; with
   // senders walking their targets in rotated order (below) it beats pull
   // from ~32 MiB at K=2 and K=4 (profiles/r01_sweep_k4_push.txt).
-  bool PushCopies(const std::vector<int>& g, uint64_t bytes) const {
+  bool PushCopies(const std::vector<int>& g, uint64_t bytes, uint64_t min_bytes = ~0ull) const {
+    if (min_bytes == ~0ull) min_bytes = ctx->push_min_bytes;
     std::set<int> gpus;
     for (int d : g) gpus.insert(ctx->slot_rank[d]);
-    return gpus.size() >= 2 && static_cast<int>(gpus.size()) <= ctx->push_max_gpus && bytes >= ctx->push_min_bytes &&
+    return gpus.size() >= 2 && static_cast<int>(gpus.size()) <= ctx->push_max_gpus && bytes >= min_bytes &&
            bytes > 0;
   }
-  bool PushSums(const std::vector<int>& g, uint64_t bytes) const {
-    return PushCopies(g, bytes) && ctx->scratch_regions >= static_cast<int>(g.size());
+  bool PushSums(const std::vector<int>& g, uint64_t bytes, uint64_t min_bytes = ~0ull) const {
+    return PushCopies(g, bytes, min_bytes) && ctx->scratch_regions >= static_cast<int>(g.size());
   }
 
   static void Add(std::vector<ProtoTask>& out, int owner, const std::vector<Range>& ranges,
@@ -210,7 +211,8 @@ struct Compiler {
   // results stored to dst_of(j).
   template <typename DstOf>
   void Sums(StepTasks& out, const std::vector<int>& g, const std::vector<int>& owner_idx,
-            const std::vector<std::vector<Range>>& parts, bool push, DstOf dst_of) {
+            const std::vector<std::vector<Range>>& parts, bool push, DstOf dst_of,
+            uint64_t wave_bytes = ~0ull) {
     const int n = static_cast<int>(g.size());
     for (size_t j = 0; j < owner_idx.size(); ++j) {
       const int p = owner_idx[j];
@@ -230,7 +232,7 @@ struct Compiler {
       for (int m : g) pull_src.push_back(Buf(m));
       int wave = 0;
       for (const Range& part : parts[j]) {
-        for (const Range& r : Waves(part)) {
+        for (const Range& r : Waves(part, wave_bytes)) {
           ProtoTask b{g[p], r, {}, dst_of(j)};
           b.wave = wave;
           for (int i = 0; i < n; ++i) {
@@ -458,7 +460,8 @@ struct Compiler {
         // chunk flags with the root pulling the results — slower.)
         const std::vector<Ref> root{Buf(g[0])};
         int mc = -1;
-        const int mode = n >= 3 ? ctx->reduce_mode : kReducePull;
+        int mode = n >= 3 ? ctx->reduce_mode : kReducePull;
+        if (mode == kReduceAuto) mode = TotalBytes(ranges) >= ctx->reduce_push_min_bytes ? kReducePush : kReducePull;
         if ((mode == kReduceNvls || mode == kReduceNvlsRoot) && NvlsEligible(g, TotalBytes(ranges)) &&
             !EnsureMulticast(ctx, g, &mc).ok()) {
           ctx->nvls = false;  // consistent P2P fallback on every rank (see AllReduce)
@@ -486,7 +489,8 @@ struct Compiler {
           for (int i = 1; i < n; ++i) owners.push_back(i);
         }
         Sums(out, g, owners, SplitEven(ranges, static_cast<int>(owners.size())),
-             mode == kReducePush && PushSums(g, TotalBytes(ranges)), [&](size_t) { return root; });
+             mode == kReducePush && PushSums(g, TotalBytes(ranges), 0), [&](size_t) { return root; },
+             ctx->reduce_wave_bytes);
         for (int r : rows) Vid(g[0], r) = next_id++;
         break;
       }

@@ -476,6 +476,26 @@ def test_reduce_mode_option_validated():
     ctx = executor.Context.virtual(4, [0, 1, 2, 3], 4)
     with pytest.raises(ExecError):
         ctx.set_option("reduce_mode", 7)
+    with pytest.raises(ExecError):
+        ctx.set_option("reduce_mode", -2)
+
+
+def test_reduce_auto_policy_by_size():
+    """Default Reduce policy (reduce_mode -1): groups of >= 3 members pull
+    below reduce_push_min_bytes and push (waves) from there; 2-member groups
+    are always pulled by the root."""
+    from paper_2110_10548_b200.planner import LoweredProgram
+    ctx = executor.Context.virtual(4, [0, 1, 2, 3], 4)
+    ctx.set_option("ll_max_bytes", 0)
+    ctx.set_option("reduce_push_min_bytes", 1 << 20)
+    prog = LoweredProgram(steps=[(3, [[0, 1, 2, 3]])])
+    small = ctx.compile(prog, (1 << 19) // 2, numeric.BF16).describe()
+    big = ctx.compile(prog, (4 << 20) // 2, numeric.BF16).describe()
+    modes = lambda d: {t["mode"] for rk in d["steps"][0]["ranks"] for t in rk["tasks"]}
+    assert modes(small) == {0}
+    assert {3, 4} <= modes(big)
+    ctx.set_option("reduce_mode", 0)
+    assert modes(ctx.compile(prog, (4 << 20) // 2, numeric.BF16).describe()) == {0}
 
 
 @pytest.mark.parametrize("mapping", ["one_per_gpu", "two_gpus", "interleaved2"])
@@ -491,6 +511,7 @@ def test_push_waves_bit_exact_and_ordered(mapping, reduce_mode):
     ctx.set_option("ll_max_bytes", 0)
     ctx.set_option("push_min_bytes", 0)
     ctx.set_option("push_wave_bytes", 16 << 10)
+    ctx.set_option("reduce_wave_bytes", 16 << 10)
     ctx.set_option("reduce_mode", reduce_mode)
     N = (1 << 17) + 3
     waves = 0
