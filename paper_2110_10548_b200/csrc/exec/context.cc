@@ -107,6 +107,7 @@ void AssignPositions(Context* ctx) {
     if (const char* env = std::getenv("RS_LL_CAPACITY")) ctx->ll_capacity = std::strtoull(env, nullptr, 10) & ~7ull;
     if (const char* env = std::getenv("RS_LL_MAX_BYTES")) ctx->ll_max_bytes = std::strtoull(env, nullptr, 10);
   }
+  if (const char* env = std::getenv("RS_RECV_PIECE")) ctx->recv_piece_bytes = std::strtoull(env, nullptr, 10);
   if (const char* env = std::getenv("RS_FLAG_CHUNK")) {
     const uint64_t c = std::strtoull(env, nullptr, 10) & ~15ull;
     if (c >= (16u << 10)) ctx->flag_chunk = c;

@@ -80,6 +80,7 @@ struct StepArgs {
   uint64_t timeout_ns;
   uint64_t ll_parity_stride;  // bytes between the two parity regions of an LL block
   uint32_t flag_chunk;        // push-variant chunk (bytes per flag)
+  uint32_t recv_piece;        // push reducing piece (divides flag_chunk)
   uint32_t local_only;        // single-rank context: sources are read-only for the launch (.nc loads)
   uint32_t wide_loads;        // cross-GPU pull sums load every source before adding (VectorChunkWide)
   uint32_t solo;              // profiling builds only (RS_PROFILING_AIDS): skip every cross-GPU wait

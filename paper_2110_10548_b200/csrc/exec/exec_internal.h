@@ -160,6 +160,11 @@ class Context {
   std::vector<size_t> flag_offset;  // per rank: push-variant chunk flags (after the LL area)
   std::vector<uint64_t> flag_bytes;
   uint64_t flag_chunk = kFlagChunk;  // push-variant chunk (RS_FLAG_CHUNK at creation)
+  // Push reducing pieces (RS_RECV_PIECE; a divisor of flag_chunk, else the
+  // chunk itself): a 64 MiB AllReduce at K=4 has 64 reducing chunks per GPU
+  // for 148 CTAs, each storing to 4 destinations — smaller pieces keep every
+  // CTA busy in the result phase.
+  uint64_t recv_piece_bytes = 64u << 10;
   ExchangeFn exchange = nullptr;  // host all-gather (multi-process NVLS setup)
   void* exchange_user = nullptr;
   std::map<std::vector<int>, std::unique_ptr<McGroup>> mc_groups;
@@ -209,6 +214,7 @@ class Plan {
   int unroll = 4;      // 4 or 8 vectors in flight per thread per source
   int max_ctas = 0;    // 0 = resident capacity
   int ctas_per_sm = 0;  // resident capacity for (dtype, threads, unroll); 0 = recompute
+  uint32_t recv_piece = kFlagChunk;  // effective push reducing piece of this plan
   bool dynamic_pieces = true;  // push phases take pieces from an atomic queue (option / env RS_DYNAMIC_PIECES)
   bool wide_loads = true;  // cross-GPU pull sums: all sources in flight (option "wide_loads", env RS_WIDE_LOADS)
   // Launch phases, one per program step (every variant — pull, push with

@@ -573,7 +573,7 @@ Ref NullRef() { return Ref{-1, kNullRegion}; }
 // Push-variant tasks: a landing task is its vector body only; a reducing
 // task is its vector body (chunk flags appended to the pointer table) plus
 // edges that pull like the default variant.
-void LayFlagged(RankStep& rs, const ProtoTask& t, uint64_t chunk) {
+void LayFlagged(RankStep& rs, const ProtoTask& t, uint64_t chunk, uint64_t recv_piece) {
   const uint64_t a = (t.range.lo + 15) & ~uint64_t{15};
   const uint64_t b = t.range.hi & ~uint64_t{15};
   auto scalar = [&](uint64_t lo, uint64_t hi) {
@@ -629,7 +629,7 @@ void LayFlagged(RankStep& rs, const ProtoTask& t, uint64_t chunk) {
     rs.ptr_refs.insert(rs.ptr_refs.end(), t.src.begin(), t.src.end());
     rs.ptr_refs.insert(rs.ptr_refs.end(), t.dst.begin(), t.dst.end());
     for (int f : t.src_flag) rs.ptr_refs.push_back(f >= 0 ? FlagRef(f) : NullRef());
-    rs.npieces += static_cast<uint32_t>((b - a + chunk - 1) / chunk);
+    rs.npieces += static_cast<uint32_t>((b - a + recv_piece - 1) / recv_piece);
     rs.tasks.push_back(task);
   }
   scalar(b, t.range.hi);
@@ -669,9 +669,9 @@ bool PlaceFlags(const Context& ctx, std::vector<RankStep>& phase) {
 }
 
 // Appends `t` to its owner rank's phase: vector body + scalar head/tail.
-void Lay(RankStep& rs, const ProtoTask& t, uint32_t piece_bytes, uint64_t flag_chunk = 0) {
+void Lay(RankStep& rs, const ProtoTask& t, uint32_t piece_bytes, uint64_t flag_chunk = 0, uint64_t recv_piece = 0) {
   if (t.flag_send >= 0 || !t.src_flag.empty()) {
-    LayFlagged(rs, t, flag_chunk);
+    LayFlagged(rs, t, flag_chunk, recv_piece ? recv_piece : flag_chunk);
     return;
   }
   auto push = [&](uint64_t lo, uint64_t hi, bool vec) {
@@ -943,6 +943,10 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
   if (const char* v = std::getenv("RS_MAX_CTAS")) plan->max_ctas = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("RS_WIDE_LOADS")) plan->wide_loads = std::atoi(v) != 0;
   if (const char* v = std::getenv("RS_DYNAMIC_PIECES")) plan->dynamic_pieces = std::atoi(v) != 0;
+  {
+    const uint64_t rp = ctx->recv_piece_bytes;
+    plan->recv_piece = static_cast<uint32_t>(rp >= 16 && rp % 16 == 0 && ctx->flag_chunk % rp == 0 ? rp : ctx->flag_chunk);
+  }
 
   // 2./3. Tasks per step, laid out into one launch phase per step.
   Compiler comp(ctx, elems, es, dtype);
@@ -1028,7 +1032,7 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
     for (const ProtoTask& t : list) {
       AddTraffic(plan->phases.back(), *ctx, t);
       RankStep& rs = plan->phases.back()[ctx->slot_rank[t.owner]];
-      Lay(rs, t, rs.piece_bytes, ctx->flag_chunk);
+      Lay(rs, t, rs.piece_bytes, ctx->flag_chunk, plan->recv_piece);
     }
     if (comp.next_flag > 0 && !PlaceFlags(*ctx, plan->phases.back())) {
       return absl::InternalError("push variant: flag area overflow");

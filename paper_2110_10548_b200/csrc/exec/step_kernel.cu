@@ -244,7 +244,7 @@ __device__ __forceinline__ void VectorChunk(const Task& t, void* const* ptrs, ui
 // nsrc (<= kS) sources' kU vectors are loaded before the first add, so a
 // chunk costs one round trip instead of nsrc serialized ones; the sum is
 // still taken in source (group) order. Remote loads are weak ld.global.
-template <int DT, int kS, int kU>
+template <int DT, int kS, int kU, bool kCoherent = false>
 __device__ __forceinline__ void VectorChunkWide(const Task& t, void* const* ptrs, uint64_t begin,
                                                 uint64_t end) {
   using Acc = typename AccOf<DT>::T;
@@ -266,7 +266,7 @@ __device__ __forceinline__ void VectorChunkWide(const Task& t, void* const* ptrs
       const char* si = static_cast<const char*>(src[i]);
 #pragma unroll
       for (int u = 0; u < kU; ++u)
-        if (ok[u]) raw[i][u] = LoadStream<false>(si + off[u]);
+        if (ok[u]) raw[i][u] = kCoherent ? LoadCoherent(si + off[u]) : LoadStream<false>(si + off[u]);
     }
   }
   Acc acc[kU];
@@ -749,24 +749,41 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
       // Push variant, one flag_chunk piece: land it and raise its flag, or
       // wait for every pushed source's flag and reduce it.
       const uint32_t k = p - t.piece_begin;
-      const uint64_t begin = t.lo + static_cast<uint64_t>(k) * a.flag_chunk;
-      const uint64_t end = min(t.hi, begin + a.flag_chunk);
       const uint64_t chunk = static_cast<uint64_t>(blockDim.x) * kUnroll * 16u;
       void* const* flags = a.ptrs + t.ptr_begin + t.nsrc + t.ndst;
       if (t.mode == kModeFlagRecv) {
+        // Reducing pieces are recv_piece bytes (a divisor of flag_chunk), so
+        // the reduce work of a mid-size step spreads over every CTA; each
+        // waits for the flags of the landing chunk that contains it.
+        const uint64_t begin = t.lo + static_cast<uint64_t>(k) * a.recv_piece;
+        const uint64_t end = min(t.hi, begin + a.recv_piece);
+        const uint64_t fk = (begin - t.lo) / a.flag_chunk;
 #ifdef RS_PROFILING_AIDS
         const bool skip_wait = a.solo != 0;
 #else
         constexpr bool skip_wait = false;
 #endif
         if (threadIdx.x < t.nsrc && flags[threadIdx.x] && !skip_wait) {
-          WaitAtLeast(static_cast<const uint64_t*>(flags[threadIdx.x]) + k, epoch, a.timeout_ns, a.error_flag);
+          WaitAtLeast(static_cast<const uint64_t*>(flags[threadIdx.x]) + fk, epoch, a.timeout_ns, a.error_flag);
         }
         __syncthreads();
         RS_TRACE(3ull * p + 1);
-        for (uint64_t c = begin; c < end; c += chunk)
-          VectorChunk<DT, kUnroll, kNc, true>(t, a.ptrs, c, min(end, c + chunk));
+        if (a.wide_loads && t.nsrc >= 2 && t.nsrc <= 4) {
+          constexpr uint64_t kW = 2;
+          const uint64_t wchunk = static_cast<uint64_t>(blockDim.x) * kW * 16u;
+          for (uint64_t c = begin; c < end; c += wchunk)
+            VectorChunkWide<DT, 4, kW, true>(t, a.ptrs, c, min(end, c + wchunk));
+        } else if (a.wide_loads && t.nsrc > 4 && t.nsrc <= 8) {
+          const uint64_t wchunk = static_cast<uint64_t>(blockDim.x) * 16u;
+          for (uint64_t c = begin; c < end; c += wchunk)
+            VectorChunkWide<DT, 8, 1, true>(t, a.ptrs, c, min(end, c + wchunk));
+        } else {
+          for (uint64_t c = begin; c < end; c += chunk)
+            VectorChunk<DT, kUnroll, kNc, true>(t, a.ptrs, c, min(end, c + chunk));
+        }
       } else {
+        const uint64_t begin = t.lo + static_cast<uint64_t>(k) * a.flag_chunk;
+        const uint64_t end = min(t.hi, begin + a.flag_chunk);
         for (uint64_t c = begin; c < end; c += chunk)
           VectorChunk<DT, kUnroll, kNc>(t, a.ptrs, c, min(end, c + chunk));
         __syncthreads();
