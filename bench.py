@@ -43,6 +43,14 @@ ELEMS = D_BYTES // 2
 REQUESTS = [[1], [0, 1]]
 AXES = [2, 4]
 SYSTEM = os.path.join(ROOT, "configs", "b200_sock.json")
+# BASELINE.json configs 1-3: descriptor b200_sock
+# [(node,1),(socket,2),(GPU,4)], 8 program devices ("slots").
+WORKLOADS = {
+    "config1": {"axes": [2, 4], "requests": [[0]], "bytes": 64 << 20, "dtype": "f32"},
+    "config2": {"axes": [2, 4], "requests": [[1], [0, 1]], "bytes": 256 << 20, "dtype": "bf16"},
+    "config3": {"axes": [2, 2, 2], "requests": [[0], [1], [2], [0, 1], [0, 2], [1, 2]], "bytes": 64 << 20,
+                "dtype": "bf16"},
+}
 # --workload kN: K = N program devices, one per GPU (BASELINE config 4 descriptors)
 K_DESCRIPTORS = {2: "b200_flat2", 4: "b200_sock4", 8: "b200_sock"}
 
@@ -59,16 +67,19 @@ def load_peaks():
 NVLINK_PEAK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); nominal 900
 
 
-def programs():
+def programs(axes=None, requests=None, payload=None, config=None):
     from paper_2110_10548_b200 import planner
+    axes = AXES if axes is None else axes
+    requests = REQUESTS if requests is None else requests
+    payload = D_BYTES if payload is None else payload
     out = []
-    for red in REQUESTS:
-        syn = planner.synthesize(SYSTEM, AXES, red, payload_bytes=D_BYTES)
+    for red in requests:
+        syn = planner.synthesize(SYSTEM, axes, red, payload_bytes=payload)
         for mi, pl in enumerate(syn.placements):
             for pi, prog in enumerate(pl.programs):
                 n = len(pl.partition[0])
                 out.append({"request": red, "matrix": mi, "index": pi, "prog": prog, "group_size": n,
-                            "factors": pl.factors, "partition": pl.partition})
+                            "factors": pl.factors, "partition": pl.partition, "config": config})
     return out
 
 
@@ -171,12 +182,15 @@ def bench_config(workload, world, n_programs):
     if workload == "config2":
         text = ("config 2: all 754 synthesized programs (axes [2,4] on b200_sock, reduce {1} "
                 "and {0,1}), 8 slots x 256 MiB bf16")
+    elif workload == "config3":
+        text = (f"config 3: all {n_programs} synthesized programs (axes [2,2,2] on b200_sock, every single-axis "
+                f"and two-axis request), 8 slots x 64 MiB bf16")
     else:
         text = (f"config 4 K={K_SLOTS}: all {n_programs} programs of {os.path.basename(SYSTEM)} axes {AXES}, "
                 f"{K_SLOTS} slots x 256 MiB bf16")
     return {"workload": text, "slots_per_gpu": K_SLOTS // world, "programs": n_programs,
             "parallelism": f"{world} GPU(s), slots block-distributed",
-            "l2": "inputs larger than L2 (8 x 256 MiB)"}
+            "l2": f"inputs larger than L2 (8 x {D_BYTES >> 20} MiB)"}
 
 
 class _Prog:
@@ -278,8 +292,11 @@ def main():
     ap.add_argument("--e2e-serial", action="store_true", help="e2e without overlapping copies across steps")
     ap.add_argument("--no-graph", action="store_true", help="timed steps launch every program eagerly")
     ap.add_argument("--programs-out", default=None, help="write per-program device times (JSON)")
-    ap.add_argument("--workload", default="config2", choices=["config2", "kN"],
-                    help="config2: BASELINE config 2 (8 slots); kN: K = N slots, one per GPU")
+    ap.add_argument("--workload", default="config2", choices=["config2", "config3", "kN"],
+                    help="config2: BASELINE config 2 (8 slots); config3: BASELINE config 3 (8 slots, 64 MiB); "
+                         "kN: K = N slots, one per GPU")
+    ap.add_argument("--no-rescore-all", action="store_true",
+                    help="skip timing the programs of the other configs (1-3) for the simulator rescoring")
     ap.add_argument("--no-nvls", action="store_true", help="P2P kernels only (bit-exact everywhere)")
     ap.add_argument("--ranks-per-gpu", type=int, default=1,
                     help="dry run of an N-GPU launch on fewer GPUs: R ranks share each GPU (time-sliced; the "
@@ -290,7 +307,11 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
-    global K_SLOTS, SYSTEM, AXES, REQUESTS
+    global K_SLOTS, SYSTEM, AXES, REQUESTS, D_BYTES, ELEMS, DTYPE
+    if args.workload in WORKLOADS:
+        wl = WORKLOADS[args.workload]
+        AXES, REQUESTS, D_BYTES, DTYPE = wl["axes"], wl["requests"], wl["bytes"], wl["dtype"]
+        ELEMS = D_BYTES // (2 if DTYPE == "bf16" else 4)
     if args.workload == "kN":
         from paper_2110_10548_b200 import planner as _pl
         K_SLOTS = args.gpus
@@ -331,7 +352,7 @@ def main():
 
     ctx = make_ctx()
 
-    entries = programs()
+    entries = programs(config=args.workload)
     # synthetic inputs for the slots this rank hosts (seed 1000+d)
     gen = torch.Generator(device=dev)
     for d in ctx.hosted_slots:
@@ -510,21 +531,16 @@ def main():
     speedups = [i["speedup_vs_nccl"] for i in inst_list if "speedup_vs_nccl" in i]
     speedup_vs_nccl = round(float(statistics.geometric_mean(speedups)), 4) if speedups else None
     from paper_2110_10548_b200 import rescore
-    resc = rescore.topk([{"instance": (tuple(e["request"]), e["matrix"]), "index": e["index"],
-                          "sim_seconds": e["prog"].seconds, "measured_us": us, "text": e["prog"].text}
-                         for e, us in zip(entries, prog_us)])
-    sim_topk = {"instances": resc["instances"], "top_k": resc["top_k"], "top_k_tie_aware": resc["top_k_tie_aware"],
-                "spearman": resc["spearman"]}
-    # The B200-calibrated model (rs_plan_predict_us) on the same instances:
-    # per launch, measured latency + the plan's own link / HBM bytes at the
-    # measured rates (local launches ~3 us, cross-GPU ~8 us incl. handshake).
+    # Config 5 rows (reference Simulate vs measured, and the B200-calibrated
+    # model rs_plan_predict_us: per launch, measured latency + the plan's own
+    # link / HBM bytes at the measured rates; local launches ~3 us,
+    # cross-GPU ~8 us incl. handshake). Configs other than this workload's are
+    # timed at the end (outside every timed region) and added.
     cal_args = dict(launch_us=3.0, link_gbs=650.0, hbm_gbs=5967.0) if world == 1 else \
         dict(launch_us=8.0, link_gbs=650.0, hbm_gbs=5967.0)
-    cal = rescore.topk([{"instance": (tuple(e["request"]), e["matrix"]), "index": e["index"],
-                         "sim_seconds": p.predict_us(**cal_args), "measured_us": us, "text": e["prog"].text}
-                        for e, p, us in zip(entries, plans, prog_us)])
-    cal_topk = {"instances": cal["instances"], "top_k": cal["top_k"], "top_k_tie_aware": cal["top_k_tie_aware"],
-                "spearman": cal["spearman"], "model": cal_args}
+    resc_rows = [{"instance": (args.workload, tuple(e["request"]), e["matrix"]), "index": e["index"],
+                  "sim_seconds": e["prog"].seconds, "cal_us": p.predict_us(**cal_args), "measured_us": us,
+                  "text": e["prog"].text} for e, p, us in zip(entries, plans, prog_us)]
 
     # End to end through the C-ABI from pinned HOST memory: every step
     # uploads the hosted slots' inputs (rs_ctx_upload), runs the step's
@@ -621,13 +637,66 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(entries)
+        cpu = cpu_baseline(entries, args.workload)
+
+    # Config 5 over configs 1-3 (BASELINE.json): time every program of the
+    # other configs (one warm run, then two back-to-back runs per program,
+    # max over ranks) in a 64 MiB context, outside every timed region.
+    rescore_configs = [args.workload] if args.workload in WORKLOADS else []
+    if args.workload in WORKLOADS and not args.no_rescore_all:
+        barrier()
+        extra_ctx = executor.Context.from_process_group(K_SLOTS, slot_rank, 64 << 20) if multi else \
+            executor.Context.local(K_SLOTS, [device] * K_SLOTS, 64 << 20)
+        for name in ("config1", "config2", "config3"):
+            wl = WORKLOADS[name]
+            if name == args.workload or wl["bytes"] > (64 << 20):
+                continue
+            es = 2 if wl["dtype"] == "bf16" else 4
+            ents = programs(wl["axes"], wl["requests"], wl["bytes"], config=name)
+            ps = [extra_ctx.compile(e["prog"], wl["bytes"] // es, wl["dtype"]) for e in ents]
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in ps]
+            barrier()
+            for p, (a, b) in zip(ps, evs):
+                p.run()
+                a.record(stream)
+                p.run()
+                p.run()
+                b.record(stream)
+            barrier()
+            us = [a.elapsed_time(b) * 1e3 / 2 for a, b in evs]
+            if multi:
+                t = torch.tensor(us, device=dev, dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                us = t.tolist()
+            resc_rows += [{"instance": (name, tuple(e["request"]), e["matrix"]), "index": e["index"],
+                           "sim_seconds": e["prog"].seconds, "cal_us": p.predict_us(**cal_args), "measured_us": u,
+                           "text": e["prog"].text} for e, p, u in zip(ents, ps, us)]
+            for p in ps:
+                p.close()
+            rescore_configs.append(name)
+        barrier()
+        extra_ctx.close()
+
+    def topk_block(key, extra):
+        res = rescore.topk([dict(r, sim_seconds=r[key]) for r in resc_rows])
+        by_cfg = {}
+        for c in rescore_configs:
+            sub = rescore.topk([dict(r, sim_seconds=r[key]) for r in resc_rows if r["instance"][0] == c])
+            by_cfg[c] = {"instances": sub["instances"], "top_k": sub["top_k"],
+                         "top_k_tie_aware": sub["top_k_tie_aware"], "spearman": sub["spearman"]}
+        out = {"instances": res["instances"], "configs": rescore_configs, "top_k": res["top_k"],
+               "top_k_tie_aware": res["top_k_tie_aware"], "spearman": res["spearman"], "by_config": by_cfg}
+        out.update(extra)
+        return out
+
+    sim_topk = topk_block("sim_seconds", {"model": "reference Simulate (ring, b200_sock bandwidths)"})
+    cal_topk = topk_block("cal_us", {"model": cal_args})
 
     if args.programs_out and rank == 0:
         with open(args.programs_out, "w") as f:
-            json.dump([{"request": e["request"], "matrix": e["matrix"], "index": e["index"], "text": e["prog"].text,
-                        "sim_seconds": e["prog"].seconds, "calibrated_us": p.predict_us(**cal_args), "measured_us": us}
-                       for e, p, us in zip(entries, plans, prog_us)], f)
+            json.dump([{"config": r["instance"][0], "request": list(r["instance"][1]), "matrix": r["instance"][2],
+                        "index": r["index"], "text": r["text"], "sim_seconds": r["sim_seconds"],
+                        "calibrated_us": r["cal_us"], "measured_us": r["measured_us"]} for r in resc_rows], f)
 
     if rank == 0:
         line = {
@@ -667,7 +736,7 @@ def main():
         dist.destroy_process_group()
 
 
-def cpu_baseline(entries):
+def cpu_baseline(entries, workload="config2"):
     """The C oracle on this host's cores over a bounded sample (2 programs
     of config 2 at full size), reported beside the GPU number."""
     try:
@@ -691,8 +760,8 @@ def cpu_baseline(entries):
         done += 1
     return {"value": round(b / t / 1e9, 3), "unit": "GB/s", "cores": threads, "cpu_model": cpu_model(),
             "kind": "port",
-            "sample": f"{done} config-2 programs (every 97th of the 754, in order) at full size "
-                      f"(8 x 256 MiB bf16), ~10 s of CPU time",
+            "sample": f"{done} {workload} programs (every 97th of the {len(entries)}, in order) at full size "
+                      f"({K_SLOTS} x {D_BYTES >> 20} MiB bf16), ~10 s of CPU time",
             "seconds": round(t, 2)}
 
 
