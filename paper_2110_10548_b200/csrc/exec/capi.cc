@@ -315,8 +315,12 @@ int rs_plan_set_option(rs_plan* plan, const char* key, long long value) {
     plan->impl->wide_loads = value != 0;
   } else if (k == "dynamic_pieces") {
     plan->impl->dynamic_pieces = value != 0;
+  } else if (k == "pdl") {
+    plan->impl->pdl = value != 0;
+  } else if (k == "local_wide") {
+    plan->impl->local_wide = value != 0;
   } else {
-    return Bad("unknown option (unroll | threads | max_ctas | wide_loads | dynamic_pieces)");
+    return Bad("unknown option (unroll | threads | max_ctas | wide_loads | dynamic_pieces | pdl | local_wide)");
   }
   plan->impl->ctas_per_sm = 0;
   return RS_OK;

@@ -83,6 +83,8 @@ struct StepArgs {
   uint32_t recv_piece;        // push reducing piece (divides flag_chunk)
   uint32_t local_only;        // single-rank context: sources are read-only for the launch (.nc loads)
   uint32_t wide_loads;        // cross-GPU pull sums load every source before adding (VectorChunkWide)
+  uint32_t pdl;               // launched with programmatic stream serialization
+  uint32_t local_wide;        // one-GPU sums load every source before adding
   uint32_t solo;              // profiling builds only (RS_PROFILING_AIDS): skip every cross-GPU wait
   uint64_t* trace;            // profiling builds only: %globaltimer stamps per piece (RS_TRACE_PTR)
 };

@@ -215,7 +215,9 @@ class Plan {
   int max_ctas = 0;    // 0 = resident capacity
   int ctas_per_sm = 0;  // resident capacity for (dtype, threads, unroll); 0 = recompute
   uint32_t recv_piece = kFlagChunk;  // effective push reducing piece of this plan
-  bool dynamic_pieces = true;  // push phases take pieces from an atomic queue (option / env RS_DYNAMIC_PIECES)
+  bool dynamic_pieces = true;
+  bool pdl = false;  // programmatic dependent launch of every step (option "pdl", env RS_PDL): measured neutral
+  bool local_wide = false;  // one-GPU sums: all sources in flight (option "local_wide", env RS_LOCAL_WIDE)  // push phases take pieces from an atomic queue (option / env RS_DYNAMIC_PIECES)
   bool wide_loads = true;  // cross-GPU pull sums: all sources in flight (option "wide_loads", env RS_WIDE_LOADS)
   // Launch phases, one per program step (every variant — pull, push with
   // chunk flags, one-shot, NVLS — runs its step in a single launch).

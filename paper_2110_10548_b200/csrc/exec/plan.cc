@@ -943,6 +943,8 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
   if (const char* v = std::getenv("RS_MAX_CTAS")) plan->max_ctas = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("RS_WIDE_LOADS")) plan->wide_loads = std::atoi(v) != 0;
   if (const char* v = std::getenv("RS_DYNAMIC_PIECES")) plan->dynamic_pieces = std::atoi(v) != 0;
+  if (const char* v = std::getenv("RS_PDL")) plan->pdl = std::atoi(v) != 0;
+  if (const char* v = std::getenv("RS_LOCAL_WIDE")) plan->local_wide = std::atoi(v) != 0;
   {
     const uint64_t rp = ctx->recv_piece_bytes;
     plan->recv_piece = static_cast<uint32_t>(rp >= 16 && rp % 16 == 0 && ctx->flag_chunk % rp == 0 ? rp : ctx->flag_chunk);

@@ -76,6 +76,8 @@ void BuildLaunches(Plan* plan) {
 #endif
       a.local_only = ctx->world == 1 ? 1u : 0u;
       a.wide_loads = plan->wide_loads ? 1u : 0u;
+      a.pdl = plan->pdl ? 1u : 0u;
+      a.local_wide = plan->local_wide ? 1u : 0u;
       a.signal_done = rsx.signal_done ? 1u : 0u;
       a.wait_lag = static_cast<uint32_t>(plan->phase_lag[ph]);
       a.epoch_base = reinterpret_cast<uint64_t*>(rank.heap + kEpochOffset);

@@ -244,7 +244,7 @@ __device__ __forceinline__ void VectorChunk(const Task& t, void* const* ptrs, ui
 // nsrc (<= kS) sources' kU vectors are loaded before the first add, so a
 // chunk costs one round trip instead of nsrc serialized ones; the sum is
 // still taken in source (group) order. Remote loads are weak ld.global.
-template <int DT, int kS, int kU, bool kCoherent = false>
+template <int DT, int kS, int kU, bool kCoherent = false, bool kNc = false>
 __device__ __forceinline__ void VectorChunkWide(const Task& t, void* const* ptrs, uint64_t begin,
                                                 uint64_t end) {
   using Acc = typename AccOf<DT>::T;
@@ -266,7 +266,7 @@ __device__ __forceinline__ void VectorChunkWide(const Task& t, void* const* ptrs
       const char* si = static_cast<const char*>(src[i]);
 #pragma unroll
       for (int u = 0; u < kU; ++u)
-        if (ok[u]) raw[i][u] = kCoherent ? LoadCoherent(si + off[u]) : LoadStream<false>(si + off[u]);
+        if (ok[u]) raw[i][u] = kCoherent ? LoadCoherent(si + off[u]) : LoadStream<kNc>(si + off[u]);
     }
   }
   Acc acc[kU];
@@ -827,6 +827,22 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
           done = true;
         }
       }
+      if constexpr (kNc && kUnroll == 8) {
+        // one GPU: every source's loads in flight at once (A/B: RS_LOCAL_WIDE)
+        if (a.local_wide && t.nsrc >= 2 && t.nsrc <= 4) {
+          constexpr uint64_t kW = 4;
+          const uint64_t wchunk = static_cast<uint64_t>(blockDim.x) * kW * 16u;
+          for (uint64_t c = begin; c < end; c += wchunk)
+            VectorChunkWide<DT, 4, kW, false, true>(t, a.ptrs, c, min(end, c + wchunk));
+          done = true;
+        } else if (a.local_wide && t.nsrc > 4 && t.nsrc <= 8) {
+          constexpr uint64_t kW = 2;
+          const uint64_t wchunk = static_cast<uint64_t>(blockDim.x) * kW * 16u;
+          for (uint64_t c = begin; c < end; c += wchunk)
+            VectorChunkWide<DT, 8, kW, false, true>(t, a.ptrs, c, min(end, c + wchunk));
+          done = true;
+        }
+      }
       if (!done) {
         for (uint64_t c = begin; c < end; c += chunk) VectorChunk<DT, kUnroll, kNc>(t, a.ptrs, c, min(end, c + chunk));
       }
@@ -891,6 +907,13 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
 
 template <int DT, int kUnroll, bool kLL, bool kNc>
 __global__ void __launch_bounds__(512, kUnroll == 4 ? 2 : 1) StepKernel(const __grid_constant__ StepArgs a) {
+  // Programmatic dependent launch: the next step's grid may be scheduled as
+  // soon as this one runs (its launch latency hides under this step), but
+  // every step first waits here until the previous grid on the stream has
+  // completed and its memory is visible — the same ordering as a plain
+  // stream launch. (No-ops for launches without the PDL attribute.)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // Run base epoch (device resident; advanced by the previous run's last step).
   const uint64_t base = a.nsignal ? *reinterpret_cast<volatile uint64_t*>(a.epoch_base) : 0;
   Phase<DT, kUnroll, kLL, kNc>(a, base);
@@ -912,15 +935,33 @@ int Occupancy(int dtype, int threads) {
   return blocks;
 }
 
+template <int DT, int U, bool LL, bool NC>
+cudaError_t LaunchOne(const StepArgs& a, int grid, int block, cudaStream_t stream, bool pdl) {
+  if (!pdl) {
+    StepKernel<DT, U, LL, NC><<<grid, block, 0, stream>>>(a);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, StepKernel<DT, U, LL, NC>, a);
+}
+
 template <int U, bool LL, bool NC>
 cudaError_t Launch(const StepArgs& a, int grid, int block, cudaStream_t stream) {
+  const bool pdl = a.pdl != 0;
   switch (a.dtype) {
-    case RS_F32: StepKernel<RS_F32, U, LL, NC><<<grid, block, 0, stream>>>(a); break;
-    case RS_BF16: StepKernel<RS_BF16, U, LL, NC><<<grid, block, 0, stream>>>(a); break;
-    case RS_I32: StepKernel<RS_I32, U, LL, NC><<<grid, block, 0, stream>>>(a); break;
+    case RS_F32: return LaunchOne<RS_F32, U, LL, NC>(a, grid, block, stream, pdl);
+    case RS_BF16: return LaunchOne<RS_BF16, U, LL, NC>(a, grid, block, stream, pdl);
+    case RS_I32: return LaunchOne<RS_I32, U, LL, NC>(a, grid, block, stream, pdl);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 // NVLS self-check: f32 AllReduce of [lo, hi) through the multicast address
