@@ -25,7 +25,7 @@ EXEC_HDRS    := $(wildcard $(PKG)/csrc/exec/*.h) $(wildcard $(PKG)/csrc/exec/*.c
 EXEC_OBJS    := $(patsubst $(PKG)/csrc/exec/%.cc,$(LIB)/obj/exec_%.o,$(EXEC_CC)) \
                 $(patsubst $(PKG)/csrc/exec/%.cu,$(LIB)/obj/cu_%.o,$(EXEC_CU))
 
-.PHONY: all planner exec oracle check-ref clean profiling
+.PHONY: all planner exec oracle check-ref clean profiling checked
 all: planner exec $(LIB)/synth $(LIB)/execute_example
 
 planner: $(LIB)/libredsynth_planner.a
@@ -69,6 +69,23 @@ $(LIB)/prof/cu_%.o: $(PKG)/csrc/exec/%.cu $(EXEC_HDRS)
 	$(NVCC) $(NVFLAGS) -DRS_PROFILING_AIDS $(INC) -c $< -o $@ 2> $(LIB)/prof/cu_$*.ptxas.txt || (cat $(LIB)/prof/cu_$*.ptxas.txt; false)
 
 $(LIB)/libredsynth_b200_prof.so: $(patsubst $(LIB)/obj/%,$(LIB)/prof/%,$(filter $(LIB)/obj/exec_% $(LIB)/obj/cu_%,$(EXEC_OBJS))) $(PLANNER_OBJS)
+	$(NVCC) -ccbin /usr/bin/g++ $(ARCH) -shared -o $@ $^ -Xcompiler -pthread
+
+# Checked build (never loaded by default): device-side bounds and protocol
+# assertions (task ranges within the slot region, pieces within their task,
+# no one-shot packet or push chunk flag from a later epoch). Run the GPU suite
+# with RS_LIB_PATH=$(LIB)/libredsynth_b200_checked.so.
+checked: $(LIB)/libredsynth_b200_checked.so
+
+$(LIB)/checked/exec_%.o: $(PKG)/csrc/exec/%.cc $(EXEC_HDRS)
+	@mkdir -p $(LIB)/checked
+	$(CXX) $(CXXFLAGS) -DRS_CHECKED $(INC) $(CUDA_INC) -c $< -o $@
+
+$(LIB)/checked/cu_%.o: $(PKG)/csrc/exec/%.cu $(EXEC_HDRS)
+	@mkdir -p $(LIB)/checked
+	$(NVCC) $(NVFLAGS) -DRS_CHECKED $(INC) -c $< -o $@ 2> $(LIB)/checked/cu_$*.ptxas.txt || (cat $(LIB)/checked/cu_$*.ptxas.txt; false)
+
+$(LIB)/libredsynth_b200_checked.so: $(patsubst $(LIB)/obj/%,$(LIB)/checked/%,$(filter $(LIB)/obj/exec_% $(LIB)/obj/cu_%,$(EXEC_OBJS))) $(PLANNER_OBJS)
 	$(NVCC) -ccbin /usr/bin/g++ $(ARCH) -shared -o $@ $^ -Xcompiler -pthread
 
 $(LIB)/execute_example: examples/execute_program.cc $(LIB)/libredsynth_b200.so

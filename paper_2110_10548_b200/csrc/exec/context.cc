@@ -353,8 +353,12 @@ absl::Status Synchronize(Context* ctx) {
     if (err) {
       RS_CUDA(cudaMemset(rank.heap + kErrorOffset, 0, sizeof(int)));
       if (first.ok()) {
-        first = absl::InternalError(absl::StrFormat(
-            "rank %d: inter-GPU barrier timed out (a peer never reached the step); results are invalid", r));
+        first = err == 1 ? absl::InternalError(absl::StrFormat(
+                               "rank %d: inter-GPU barrier timed out (a peer never reached the step); results are "
+                               "invalid", r))
+                         : absl::InternalError(absl::StrFormat(
+                               "rank %d: checked-build assertion %d failed in the step kernel (see the device "
+                               "printf); results are invalid", r, err));
       }
     }
   }

@@ -26,6 +26,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
+
 #include "device_types.h"
 
 namespace rs {
@@ -116,6 +118,26 @@ __device__ __forceinline__ uint64_t GlobalTimer() {
 __device__ __forceinline__ bool Failed(const int* error_flag) {
   return *reinterpret_cast<const volatile int*>(error_flag) != 0;
 }
+
+// Checked builds (make checked, RS_CHECKED): device-side bounds and protocol
+// assertions. A failed check prints once per CTA and raises the rank's error
+// flag with a code >= 2 (never a trap), which rs_ctx_synchronize reports.
+enum : int { kCheckRange = 2, kCheckLLFuture = 3, kCheckFlagFuture = 4, kCheckPiece = 5 };
+#ifdef RS_CHECKED
+__device__ __noinline__ void CheckFail(int* error_flag, int code, uint64_t x, uint64_t y) {
+  if (atomicCAS(error_flag, 0, code) == 0)
+    printf("redsynth checked build: assertion %d failed (block %d thread %d): %llu vs %llu\n", code, blockIdx.x,
+           threadIdx.x, static_cast<unsigned long long>(x), static_cast<unsigned long long>(y));
+}
+#define RS_CHECK(cond, flag, code, x, y)                  \
+  do {                                                    \
+    if (!(cond)) CheckFail((flag), (code), (x), (y));     \
+  } while (0)
+#else
+#define RS_CHECK(cond, flag, code, x, y) \
+  do {                                   \
+  } while (0)
+#endif
 
 // Spin until *flag >= target; on timeout raise the error flag and give up
 // (the data is then wrong, but the GPU is not hung; the host reports it).
@@ -420,6 +442,10 @@ __device__ __forceinline__ uint2 LoadLL(const char* p, uint32_t flag, uint64_t t
                  : "l"(p)
                  : "memory");
     if (f0 == flag && f1 == flag) break;
+    // a packet of a later epoch in this parity region: the sender ran two
+    // epochs ahead and overwrote data not yet consumed
+    RS_CHECK(static_cast<int32_t>(f0 - flag) <= 0 && static_cast<int32_t>(f1 - flag) <= 0, error_flag,
+             kCheckLLFuture, f0, flag);
     if (spin == 4096) {
       if (Failed(error_flag)) break;
       t0 = GlobalTimer();
@@ -745,6 +771,9 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
       return;
     }
     RS_TRACE(3ull * p);
+    RS_CHECK(t.lo <= t.hi && t.hi <= a.slot_limit, a.error_flag, kCheckRange, t.hi, a.slot_limit);
+    RS_CHECK(p >= t.piece_begin && (cur + 1 >= a.ntasks || p < a.tasks[cur + 1].piece_begin), a.error_flag,
+             kCheckPiece, p, t.piece_begin);
     if (t.mode == kModeFlagSend || t.mode == kModeFlagRecv) {
       // Push variant, one flag_chunk piece: land it and raise its flag, or
       // wait for every pushed source's flag and reduce it.
@@ -765,6 +794,12 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
 #endif
         if (threadIdx.x < t.nsrc && flags[threadIdx.x] && !skip_wait) {
           WaitAtLeast(static_cast<const uint64_t*>(flags[threadIdx.x]) + fk, epoch, a.timeout_ns, a.error_flag);
+          // a chunk flag of a later run: the sender re-landed this chunk before we reduced it
+          RS_CHECK(*reinterpret_cast<const volatile uint64_t*>(static_cast<const uint64_t*>(flags[threadIdx.x]) + fk) <=
+                       epoch || Failed(a.error_flag),
+                   a.error_flag, kCheckFlagFuture,
+                   *reinterpret_cast<const volatile uint64_t*>(static_cast<const uint64_t*>(flags[threadIdx.x]) + fk),
+                   epoch);
         }
         __syncthreads();
         RS_TRACE(3ull * p + 1);
