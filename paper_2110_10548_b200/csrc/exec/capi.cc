@@ -260,6 +260,8 @@ int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value) {
     ctx->impl->nvls_min_bytes_n8 = ctx->impl->nvls_min_bytes;
   } else if (k == "ll_max_bytes") {
     ctx->impl->ll_max_bytes = value < 0 ? 0 : static_cast<uint64_t>(value);
+  } else if (k == "ll_total_bytes") {
+    ctx->impl->ll_total_bytes = value < 0 ? 0 : static_cast<uint64_t>(value);
   } else if (k == "push_wave_bytes") {
     ctx->impl->push_wave_bytes = value <= 0 ? 0 : (static_cast<uint64_t>(value) & ~15ull);
   } else if (k == "reduce_mode") {
@@ -272,7 +274,7 @@ int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value) {
   } else if (k == "reduce_wave_bytes") {
     ctx->impl->reduce_wave_bytes = value <= 0 ? 0 : (static_cast<uint64_t>(value) & ~15ull);
   } else {
-    return Bad("unknown option (push_min_bytes | barrier_timeout_ms | nvls | nvls_min_group | nvls_min_bytes | ll_max_bytes | reduce_mode | reduce_push_min_bytes | reduce_wave_bytes | push_wave_bytes)");
+    return Bad("unknown option (push_min_bytes | barrier_timeout_ms | nvls | nvls_min_group | nvls_min_bytes | ll_max_bytes | ll_total_bytes | reduce_mode | reduce_push_min_bytes | reduce_wave_bytes | push_wave_bytes)");
   }
   return RS_OK;
 }

@@ -106,6 +106,7 @@ void AssignPositions(Context* ctx) {
     ctx->ll_max_bytes = 256u << 10;
     if (const char* env = std::getenv("RS_LL_CAPACITY")) ctx->ll_capacity = std::strtoull(env, nullptr, 10) & ~7ull;
     if (const char* env = std::getenv("RS_LL_MAX_BYTES")) ctx->ll_max_bytes = std::strtoull(env, nullptr, 10);
+    if (const char* env = std::getenv("RS_LL_TOTAL_BYTES")) ctx->ll_total_bytes = std::strtoull(env, nullptr, 10);
   }
   if (const char* env = std::getenv("RS_RECV_PIECE")) ctx->recv_piece_bytes = std::strtoull(env, nullptr, 10);
   if (const char* env = std::getenv("RS_FLAG_CHUNK")) {

@@ -148,13 +148,17 @@ class Context {
   uint64_t reduce_push_min_bytes = 128ull << 20;
   uint64_t reduce_wave_bytes = 4ull << 20;
   // One-shot (LL) steps: when every cross-GPU group of a step has its members
-  // on distinct GPUs and each GPU sends any peer at most ll_max_bytes (and
-  // at most 3 * ll_max_bytes in total), the
-  // step runs as one kernel in which every owner receives its sources as
-  // flagged packets pushed into its own LL area and sums locally: no remote
-  // loads, no tail wait (latency-bound sizes). ll_capacity is fixed at
-  // creation (RS_LL_CAPACITY); ll_max_bytes is a run-time option.
+  // on distinct GPUs, each GPU sends any peer at most ll_max_bytes and at most
+  // ll_total_bytes in total (payload; packets double it), the step runs as
+  // one kernel in which every owner receives its sources as flagged packets
+  // pushed into its own LL area and sums locally: no remote loads, no tail
+  // wait (latency-bound sizes). The total cap is what binds: measured at K=4
+  // one-shot beats pull for AllReduce only at 4 KiB and for Reduce up to
+  // 16 KiB, at K=2 for AllReduce up to 16 KiB (profiles/r02_ll_budget.txt).
+  // ll_capacity is fixed at creation (RS_LL_CAPACITY); the caps are run-time
+  // options.
   uint64_t ll_capacity = 0;
+  uint64_t ll_total_bytes = 16u << 10;
   uint64_t ll_max_bytes = 0;
   std::vector<size_t> ll_offset;  // per rank: its LL area within its heap
   std::vector<size_t> flag_offset;  // per rank: push-variant chunk flags (after the LL area)

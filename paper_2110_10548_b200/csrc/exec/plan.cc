@@ -743,11 +743,11 @@ bool LayLL(const Context& ctx, const std::vector<LLSpec>& specs, std::vector<Ran
       stream[key] = used;
       used += hi8(sp.range) - lo8(sp.range);
       if (used > budget) return false;
-      // Packets double the bytes and go to every receiver separately: cap a
-      // sender's total at what a K=4 one-shot AllReduce at the budget sends
-      // (3 peers), so wide groups (K=8) switch to pull earlier.
+      // Packets double the bytes and go to every receiver separately: a
+      // sender's total payload is capped (ll_total_bytes), so wide groups
+      // switch to pull earlier.
       sent_bytes[q] += hi8(sp.range) - lo8(sp.range);
-      if (sent_bytes[q] > 3 * budget) return false;
+      if (sent_bytes[q] > ctx.ll_total_bytes) return false;
     }
     if (locals > 1) return false;
   }

@@ -27,7 +27,7 @@ ROOT = os.path.dirname(HERE)
 MODE_SUM, MODE_NVLS, MODE_LL, MODE_FLAG_SEND, MODE_FLAG_RECV = 0, 1, 2, 3, 4
 VARIANTS = {
     # name: context options
-    "ll": {"ll_max_bytes": 256 << 10, "push_min_bytes": -1, "reduce_mode": 0},
+    "ll": {"ll_max_bytes": 256 << 10, "ll_total_bytes": 3 << 20, "push_min_bytes": -1, "reduce_mode": 0},
     "pull": {"ll_max_bytes": 0, "push_min_bytes": -1, "reduce_mode": 0},
     "push": {"ll_max_bytes": 0, "push_min_bytes": 0, "reduce_mode": 0},
     # Reduce over >= 3 ranks by push (stores only, chunk flags) — the other

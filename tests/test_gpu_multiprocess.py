@@ -91,6 +91,7 @@ def _worker(rank, world, port, result_dir):
         name = {2: "k2_flat", 4: "k4_sock", 8: "k8_sock"}[world]
         K, progs = golden_programs(name)
         ctx = executor.Context.from_process_group(K, list(range(K)), 4 << 20)
+        ctx.set_option("ll_total_bytes", 3 << 20)  # one-shot for every size below
         for N, dt in [(1, numeric.BF16), (777, numeric.BF16), (4096, numeric.F32), (30001, numeric.I32)]:
             es = 2 if dt == numeric.BF16 else 4
             inputs = numeric.synthetic_inputs(K, N, dt)

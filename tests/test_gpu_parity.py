@@ -244,6 +244,7 @@ def test_one_slot_per_gpu_small_k(push, ll):
     ctx = executor.Context.local(n, list(range(n)), max_bytes=64 << 20)
     ctx.set_option("push_min_bytes", 0 if push else -1)
     ctx.set_option("ll_max_bytes", (256 << 10) if ll else 0)
+    ctx.set_option("ll_total_bytes", 3 << 20)
     try:
         K, progs = golden_programs(name)
         for _, _, prog, _ in progs:
@@ -266,6 +267,7 @@ def test_one_shot_steps_repeated():
     if name is None:
         pytest.skip("GPU count without a golden set")
     ctx = executor.Context.local(n, list(range(n)), max_bytes=8 << 20)
+    ctx.set_option("ll_total_bytes", 3 << 20)
     try:
         K, progs = golden_programs(name)
         for N in (1, 13, 1001, 32 << 10):
@@ -288,6 +290,7 @@ def test_config3_programs_across_gpus(ll):
     n = min(NGPU, 4)
     ctx = executor.Context.local(8, [d * n // 8 for d in range(8)], max_bytes=8 << 20)
     ctx.set_option("ll_max_bytes", (256 << 10) if ll else 0)
+    ctx.set_option("ll_total_bytes", 3 << 20)
     try:
         for name in ("cfg3_r0", "cfg3_r1", "cfg3_r2", "cfg3_r01", "cfg3_r02", "cfg3_r12"):
             K, progs = golden_programs(name)

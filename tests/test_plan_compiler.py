@@ -34,6 +34,7 @@ def _compile(prog, K, mapping, N, dtype, push=False, ll=False):
     ctx.set_option("push_min_bytes", 0 if push else -1)
     if world > 1:
         ctx.set_option("ll_max_bytes", (256 << 10) if ll else 0)
+        ctx.set_option("ll_total_bytes", 3 << 20)
     plan = ctx.compile(prog, N, dtype)
     return ctx, plan, plan.describe()
 
@@ -319,12 +320,16 @@ def test_ll_ragged_sizes(N):
 
 def test_ll_budget_selects_variant():
     """An AllReduce of D bytes over n GPUs sends D to each peer: one-shot at
-    D <= ll_max_bytes per peer and (n-1) D <= 3 ll_max_bytes per sender,
-    pull above."""
+    D <= ll_max_bytes per peer and (n-1) D <= ll_total_bytes per sender,
+    pull above. Defaults: 256 KiB per peer, 16 KiB per sender."""
     K, progs = golden_programs("k4_flat")
     prog = progs[0][2]
     ctx = executor.Context.virtual(K, list(range(K)), K)
     ctx.set_option("push_min_bytes", -1)
+    D = (16 << 10) // 3 // 8 * 8  # default total cap, 3 peers
+    assert ctx.compile(prog, D // 4, "f32").describe()["phase_ll"] == [1]
+    assert ctx.compile(prog, (D + 64) // 4, "f32").describe()["phase_ll"] == [0]
+    ctx.set_option("ll_total_bytes", 3 << 20)
     ctx.set_option("ll_max_bytes", 64 << 10)
     assert ctx.compile(prog, (64 << 10) // 4, "f32").describe()["phase_ll"] == [1]
     assert ctx.compile(prog, (64 << 10) // 4 + 2, "f32").describe()["phase_ll"] == [0]
@@ -335,6 +340,7 @@ def test_ll_budget_selects_variant():
     K, progs = golden_programs("k8_flat")  # 7 peers: the per-sender cap binds first
     ctx = executor.Context.virtual(K, list(range(K)), K)
     ctx.set_option("ll_max_bytes", 64 << 10)
+    ctx.set_option("ll_total_bytes", 3 * (64 << 10))
     D = 3 * (64 << 10) // 7 // 8 * 8
     assert ctx.compile(progs[0][2], D // 4, "f32").describe()["phase_ll"] == [1]
     assert ctx.compile(progs[0][2], (D + 64) // 4, "f32").describe()["phase_ll"] == [0]
@@ -389,6 +395,7 @@ def test_random_slot_to_gpu_mappings(seed):
                 ctx = executor.Context.virtual(K, slot_rank, world)
                 ctx.set_option("push_min_bytes", 0 if push else -1)
                 ctx.set_option("ll_max_bytes", (256 << 10) if ll else 0)
+                ctx.set_option("ll_total_bytes", 3 << 20)
                 N = rng.choice([7, 100, 2049, 5000])
                 dtype = rng.choice([numeric.F32, numeric.BF16, numeric.I32])
                 desc = ctx.compile(prog, N, dtype).describe()

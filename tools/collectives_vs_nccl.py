@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--nvls", action="store_true", help="multicast-capable heaps (RS_NVLS=1; needed by modes 2/3)")
     ap.add_argument("--push-min-bytes", type=int, default=None, help="context push threshold (-1 = never push)")
     ap.add_argument("--wave-bytes", type=int, default=None, help="push waves (0 = one wave)")
+    ap.add_argument("--ll-max-bytes", type=int, default=None, help="one-shot budget (0 = never one-shot)")
     args = ap.parse_args()
     if args.nvls:
         os.environ["RS_NVLS"] = "1"
@@ -42,6 +43,8 @@ def main():
         ctx.set_option("push_min_bytes", args.push_min_bytes)
     if args.wave_bytes is not None:
         ctx.set_option("push_wave_bytes", args.wave_bytes)
+    if args.ll_max_bytes is not None:
+        ctx.set_option("ll_max_bytes", args.ll_max_bytes)
     g = list(range(world))
     ops = args.ops.split(",")
     modes = [int(m) for m in args.reduce_modes.split(",")]

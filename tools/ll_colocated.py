@@ -26,6 +26,7 @@ def main():
             row = {}
             for ll in (0, 256 << 10):
                 ctx.set_option("ll_max_bytes", ll)
+                ctx.set_option("ll_total_bytes", 3 << 20)
                 plan = ctx.compile(prog, nbytes // 2, "bf16")
                 row["one-shot" if ll else "pull"] = round(plan.time_us(3, 50), 2)
                 row["ll_phases" if ll else "_"] = sum(plan.describe()["phase_ll"]) if ll else None

@@ -34,6 +34,7 @@ def main():
     cases = [(4097, numeric.F32, 0, -1), (3001, numeric.BF16, 256 << 10, -1), ((1 << 20) - 3, numeric.I32, 0, 0)]
     for N, dt, ll, push in cases:
         ctx.set_option("ll_max_bytes", ll)
+        ctx.set_option("ll_total_bytes", 3 << 20)
         ctx.set_option("push_min_bytes", push)
         es = 2 if dt == numeric.BF16 else 4
         inputs = numeric.synthetic_inputs(K, N, dt)
