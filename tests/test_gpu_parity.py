@@ -330,6 +330,7 @@ def test_interleaved_variants_share_epochs():
         pytest.skip("GPU count without a golden set")
     K, progs = golden_programs(name)
     ctx = executor.Context.local(n, list(range(n)), max_bytes=8 << 20)
+    ctx.set_option("ll_total_bytes", 3 << 20)
     try:
         single = progs[0][2]
         multi = next(p for _, _, p, _ in progs if len(p.steps) >= 2)
