@@ -299,9 +299,10 @@ def main():
                     help="skip timing the programs of the other configs (1-3) for the simulator rescoring")
     ap.add_argument("--no-nvls", action="store_true", help="P2P kernels only (bit-exact everywhere)")
     ap.add_argument("--ranks-per-gpu", type=int, default=1,
-                    help="dry run of an N-GPU launch on fewer GPUs: R ranks share each GPU (time-sliced; the "
-                         "process group and the comparator use gloo, NCCL refuses shared GPUs). Readiness "
-                         "check only: the times are not N-GPU numbers")
+                    help="(refused unless 1) ranks sharing a GPU spin on each other's flags from separate "
+                         "launches, which B200 does not guarantee to co-schedule (Xid 109); the N=8 path is "
+                         "exercised by emulated ranks in one cooperative launch instead "
+                         "(tests/test_gpu_emulated_ranks.py)")
     ap.add_argument("--reduce-mode", type=int, default=None, help="executor Reduce variant (0 pull, 1 push, "
                     "2 NVLS, 3 NVLS root), for A/B runs")
     args = ap.parse_args()
@@ -331,7 +332,9 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    rpg = max(1, args.ranks_per_gpu)
+    if args.ranks_per_gpu != 1:
+        raise SystemExit("--ranks-per-gpu > 1 is refused: ranks that wait on each other must not share a GPU")
+    rpg = 1
     device = local_rank // rpg
     torch.cuda.set_device(device)
     dev = torch.device("cuda", device)

@@ -3,13 +3,10 @@ launch shape): CUDA-IPC heaps exchanged over a gloo process group, each rank
 enqueues only its own kernels and synchronises with its peers through epoch
 flags in their memory. Compared bit-exactly with the C oracle on every rank.
 
-Used two ways:
-  * every rank on cuda:0 (test_gpu_ranks_one_gpu.py) — the cross-rank
-    kernels (pull over peer pointers, one-shot LL packets, push with chunk
-    flags, IPC heaps, epoch barriers) run on a one-GPU box; the processes
-    time-slice the GPU, so it is slow but exercises exactly the code an
-    8-GPU run takes;
-  * rank r on cuda:r (test_gpu_multiprocess.py on multi-GPU boxes).
+Rank r runs on cuda:r (test_gpu_ranks_processes.py, multi-GPU boxes).
+Ranks must not share a GPU: kernels that spin on each other's flags are not
+guaranteed to be co-scheduled as separate launches (and have raised Xid 109
+on B200); one-GPU boxes use emulated ranks in one cooperative launch instead.
 
 Each case forces one variant through the context options the C-ABI exposes
 (ll_max_bytes, push_min_bytes) and checks from Plan.describe() that the
@@ -192,10 +189,6 @@ def spawn(world, tmp_path, device_of_rank, cases=None):
         with open(os.path.join(str(tmp_path), f"r{r}.json")) as f:
             out.append(json.load(f))
     return out
-
-
-def on_gpu0(_rank):
-    return 0
 
 
 def on_own_gpu(rank):

@@ -1,8 +1,9 @@
 #!/usr/bin/env python
 """Small executor workload for compute-sanitizer (memcheck / racecheck /
 synccheck): local mode (8 slots on cuda:0, every collective as HBM-local
-tasks) and, with --world 2, two processes on cuda:0 joined by CUDA IPC (the
-cross-rank pull, one-shot and push kernels with their flag protocol).
+tasks) and, with --world 2, two processes on cuda:0 and cuda:1 joined by CUDA
+IPC (the cross-rank pull, one-shot and push kernels with their flag
+protocol). (compute-sanitizer was closed on this round's GPU pool.)
 Bit-exact against the C oracle; exits non-zero on a mismatch.
   compute-sanitizer --tool memcheck --target-processes all python tools/sanitize_run.py --world 2"""
 import argparse
@@ -55,9 +56,9 @@ def main():
         cases.append({"set": "k4_sock", "K": 4, "N": 3001 if variant == "ll" else (1 << 16) + 3,
                       "dtype": numeric.BF16, "variant": variant, "stride": 40, "runs": 2, "graph": False})
     with tempfile.TemporaryDirectory() as tmp:
-        res = ranks_worker.spawn(args.world, tmp, ranks_worker.on_gpu0, cases)
+        res = ranks_worker.spawn(args.world, tmp, ranks_worker.on_own_gpu, cases)
     ok = all(r["ok"] for r in res)
-    print(f"world {args.world} on cuda:0: {'OK' if ok else 'FAILED'} used={res[0]['used']}", flush=True)
+    print(f"world {args.world}: {'OK' if ok else 'FAILED'} used={res[0]['used']}", flush=True)
     if not ok:
         for r in res:
             print(r["msg"])
