@@ -77,6 +77,18 @@ int rs_ctx_ipc_handle(rs_ctx* ctx, void* out);
 /* handles = world_size * RS_IPC_HANDLE_BYTES bytes, rank-major. */
 int rs_ctx_open_peers(rs_ctx* ctx, const void* handles);
 
+/* Validation mode: world_size (2..8) ranks emulated on ONE GPU. Every rank
+ * gets its own heap (slot buffers, scratch, flags, one-shot area) on
+ * cuda_ordinal, and each launch phase runs every rank's step kernel as ONE
+ * cooperative launch, so ranks that wait on each other's flags are
+ * co-resident (separate launches on one GPU are not guaranteed to run
+ * concurrently). Exercises the cross-rank kernels — pull over "peer"
+ * pointers, one-shot packets, push chunk flags, epoch barriers — exactly as
+ * compiled for world_size GPUs, without them; not a performance mode, no
+ * NVLS. Plans run on the stream of the first local rank. */
+int rs_ctx_create_emulated(int K, const int* slot_rank, int world_size, int cuda_ordinal, size_t max_bytes,
+                           rs_ctx** out);
+
 /* Planning-only context: no GPU, no memory. Plans compiled on it can be
  * inspected with rs_plan_describe_json but not run (CPU tests, tooling). */
 int rs_ctx_create_virtual(int K, const int* slot_rank, int world_size, rs_ctx** out);

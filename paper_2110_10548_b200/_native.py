@@ -27,7 +27,7 @@ RS_IPC_HANDLE_BYTES = 64
 # Every symbol include/redsynth_exec.h declares (checked by the CPU tests).
 EXPORTED_SYMBOLS = (
     "rs_last_error", "rs_version",
-    "rs_ctx_create", "rs_ctx_create_rank", "rs_ctx_ipc_handle", "rs_ctx_open_peers",
+    "rs_ctx_create", "rs_ctx_create_rank", "rs_ctx_ipc_handle", "rs_ctx_open_peers", "rs_ctx_create_emulated",
     "rs_ctx_create_virtual", "rs_plan_describe_json", "rs_ctx_set_option", "rs_ctx_nvls",
     "rs_ctx_set_exchange", "rs_ctx_upload", "rs_ctx_download",
     "rs_ctx_destroy", "rs_ctx_buffer", "rs_ctx_local_ranks", "rs_ctx_synchronize",
@@ -72,6 +72,7 @@ def _declare(lib):
         "rs_ctx_create_rank": (_I, [_I, _PI, _I, _I, _I, _SZ, ctypes.POINTER(_P)]),
         "rs_ctx_ipc_handle": (_I, [_P, _P]),
         "rs_ctx_create_virtual": (_I, [_I, _PI, _I, ctypes.POINTER(_P)]),
+        "rs_ctx_create_emulated": (_I, [_I, _PI, _I, _I, _SZ, ctypes.POINTER(_P)]),
         "rs_plan_describe_json": (_I, [_P, ctypes.POINTER(ctypes.c_void_p)]),
         "rs_ctx_set_option": (_I, [_P, ctypes.c_char_p, ctypes.c_longlong]),
         "rs_ctx_nvls": (_I, [_P, _PI]),

@@ -66,6 +66,15 @@ int rs_ctx_create_rank(int K, const int* slot_rank, int world_size, int rank, in
   return Report(s);
 }
 
+int rs_ctx_create_emulated(int K, const int* slot_rank, int world_size, int cuda_ordinal, size_t max_bytes,
+                           rs_ctx** out) {
+  if (!out || !slot_rank) return Bad("null argument");
+  rs::Context* c = nullptr;
+  const absl::Status s = rs::CreateEmulatedContext(K, slot_rank, world_size, cuda_ordinal, max_bytes, &c);
+  if (s.ok()) *out = new rs_ctx{c};
+  return Report(s);
+}
+
 int rs_ctx_create_virtual(int K, const int* slot_rank, int world_size, rs_ctx** out) {
   if (!out || !slot_rank) return Bad("null argument");
   rs::Context* c = nullptr;
@@ -198,7 +207,8 @@ int rs_plan_time(rs_plan* plan, int warmup, int iters, double* us) {
 
 int rs_plan_launch_count(rs_plan* plan, int* launches) {
   if (!plan || !launches) return Bad("null argument");
-  *launches = plan->impl->num_phases() * static_cast<int>(plan->impl->ctx->DrivenRanks().size());
+  const rs::Context* c = plan->impl->ctx;
+  *launches = plan->impl->num_phases() * (c->emulated ? 1 : static_cast<int>(c->DrivenRanks().size()));
   return RS_OK;
 }
 

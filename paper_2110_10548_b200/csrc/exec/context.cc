@@ -266,6 +266,47 @@ absl::Status CreateRankContext(int K, const int* slot_rank, int world, int rank,
   return absl::OkStatus();
 }
 
+absl::Status CreateEmulatedContext(int K, const int* slot_rank, int world, int ordinal, size_t max_bytes,
+                                   Context** out) {
+  absl::Status ok = CheckCommon(K, max_bytes);
+  if (!ok.ok()) return ok;
+  if (world < 2 || world > RS_MAX_RANKS) {
+    return absl::InvalidArgumentError(absl::StrFormat("world_size must be in [2, %d]", RS_MAX_RANKS));
+  }
+  if (slot_rank == nullptr) return absl::InvalidArgumentError("slot_rank is null");
+  int devices = 0;
+  RS_CUDA(cudaGetDeviceCount(&devices));
+  if (ordinal < 0 || ordinal >= devices) return absl::InvalidArgumentError("cuda_ordinal out of range");
+  auto ctx = std::make_unique<Context>();
+  ctx->K = K;
+  ctx->max_bytes = max_bytes;
+  ctx->slot_stride = RoundUp(max_bytes, kSlotAlign);
+  ctx->world = world;
+  ctx->emulated = true;
+  ReadTimeoutEnv(ctx.get());
+  ctx->slot_rank.assign(slot_rank, slot_rank + K);
+  for (int d = 0; d < K; ++d) {
+    if (slot_rank[d] < 0 || slot_rank[d] >= world) {
+      return absl::InvalidArgumentError(absl::StrFormat("slot %d: rank %d out of range", d, slot_rank[d]));
+    }
+  }
+  AssignPositions(ctx.get());
+  ctx->ranks.resize(world);
+  for (int r = 0; r < world; ++r) ctx->ranks[r].ordinal = ordinal;
+  for (int r = 0; r < world; ++r) {
+    absl::Status s = AllocateRank(ctx.get(), r);
+    if (!s.ok()) {
+      DestroyContext(ctx.release());
+      return s;
+    }
+  }
+  for (int r = 0; r < world; ++r)
+    for (int q = 0; q < world; ++q) ctx->ranks[r].view[q] = ctx->ranks[q].heap;
+  ctx->peers_open = true;
+  *out = ctx.release();
+  return absl::OkStatus();
+}
+
 absl::Status CreateVirtualContext(int K, const int* slot_rank, int world, Context** out) {
   if (K < 1 || K > 4096) return absl::InvalidArgumentError("K must be in [1, 4096]");
   if (world < 1 || world > RS_MAX_RANKS) {

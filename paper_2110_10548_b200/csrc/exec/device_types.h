@@ -101,6 +101,16 @@ constexpr uint32_t kLLPieceBytes = 32u << 10;
 constexpr uint32_t kFlagChunk = 256u << 10;  // measured: 64 KiB -3 %, 1 MiB -3 % at K=2
 
 cudaError_t LaunchStep(const StepArgs& args, int grid, int block, int unroll, cudaStream_t stream);
+
+// Emulated ranks: one cooperative launch runs every rank's share of a phase;
+// CTAs [prefix[r], prefix[r+1]) are rank r's grid (args[r]).
+struct EmulatedArgs {
+  StepArgs args[RS_MAX_RANKS];
+  uint32_t prefix[RS_MAX_RANKS + 1];
+  uint32_t nranks;
+};
+cudaError_t LaunchEmulated(const EmulatedArgs& e, bool ll, int block, cudaStream_t stream);
+int EmulatedResidentCtas(int dtype, int threads, bool ll);  // per SM
 // f32 multimem.ld_reduce + multimem.st over [lo, hi) of a multicast VA.
 cudaError_t LaunchNvlsSelfCheck(char* mc, uint64_t lo, uint64_t hi, cudaStream_t stream);
 

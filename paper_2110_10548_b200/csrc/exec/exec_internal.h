@@ -101,6 +101,11 @@ class Context {
   int self_rank = -1;  // -1: single process drives every rank
   bool peers_open = false;
   bool is_virtual = false;  // planning only: no CUDA resources (CPU tests)
+  // Emulated ranks (validation on one GPU, rs_ctx_create_emulated): every
+  // rank has its own heap on the same device and each launch phase runs all
+  // ranks' steps as one cooperative launch (co-resident CTAs), so ranks that
+  // wait on each other never depend on separate launches being co-scheduled.
+  bool emulated = false;
   std::vector<int> slot_rank;      // slot -> rank
   std::vector<int> slot_position;  // slot -> index among its rank's slots
   std::vector<Rank> ranks;
@@ -245,6 +250,8 @@ absl::Status CreateContext(int K, const int* ordinals, size_t max_bytes, Context
 absl::Status CreateRankContext(int K, const int* slot_rank, int world, int rank, int ordinal,
                                size_t max_bytes, Context** out);
 absl::Status CreateVirtualContext(int K, const int* slot_rank, int world, Context** out);
+absl::Status CreateEmulatedContext(int K, const int* slot_rank, int world, int ordinal, size_t max_bytes,
+                                   Context** out);
 absl::Status IpcHandle(Context* ctx, void* out);
 absl::Status OpenPeers(Context* ctx, const void* handles);
 absl::Status DestroyContext(Context* ctx);

@@ -90,7 +90,12 @@ void BuildLaunches(Plan* plan) {
         a.has_ll |= t.mode == kModeLL ? 1u : 0u;
         a.dynamic |= (plan->dynamic_pieces && (t.mode == kModeFlagSend || t.mode == kModeFlagRecv)) ? 1u : 0u;
       }
-      const int resident = plan->ctas_per_sm * rank.sm_count;
+      int resident = plan->ctas_per_sm * rank.sm_count;
+      if (ctx->emulated) {
+        // all ranks share one cooperative launch: split its co-resident CTAs
+        const bool ll = plan->phase_ll[ph] != 0;
+        resident = std::max(1, EmulatedResidentCtas(plan->dtype, plan->threads, ll) * rank.sm_count / R);
+      }
       int cap = plan->max_ctas > 0 ? std::min(plan->max_ctas, resident) : resident;
       if (rsx.max_grid > 0) cap = std::min<int>(cap, static_cast<int>(rsx.max_grid));
       // Pulling from >= 2 peers at once: one CTA per SM keeps fewer loads in
@@ -147,6 +152,24 @@ absl::Status RunPlan(Plan* plan, void* const* device_bufs, void* const* host_buf
   if (driven.size() == 1) {
     absl::Status st = CudaStatus(cudaSetDevice(ctx->ranks[driven[0]].ordinal), "cudaSetDevice");
     if (!st.ok()) return st;
+  }
+  if (ctx->emulated) {
+    // one cooperative launch per phase covering every rank (stream of rank 0)
+    for (int ph = 0; ph < P; ++ph) {
+      EmulatedArgs e{};
+      e.nranks = static_cast<uint32_t>(R);
+      bool ll = false;
+      for (int r = 0; r < R; ++r) {
+        const size_t k = static_cast<size_t>(ph) * R + r;
+        e.args[r] = plan->launch_args[k];
+        e.prefix[r + 1] = e.prefix[r] + static_cast<uint32_t>(plan->launch_grid[k]);
+        ll |= e.args[r].has_ll != 0;
+      }
+      absl::Status st = CudaStatus(LaunchEmulated(e, ll, plan->threads, stream_of(0)), "emulated step launch");
+      if (!st.ok()) return st;
+    }
+    if (device_bufs || host_bufs) return copy_all(false);
+    return absl::OkStatus();
   }
   for (int ph = 0; ph < P; ++ph) {
     for (size_t i = 0; i < driven.size(); ++i) {

@@ -721,10 +721,13 @@ __device__ __forceinline__ void LLReceive(const Task& t, void* const* ptrs, uint
 #endif
 
 // One launch phase of one rank: entry barrier, tasks, exit.
+// cta / ncta: this CTA's index among the rank's CTAs and their count
+// (blockIdx.x / gridDim.x, except in emulated-rank launches).
 template <int DT, int kUnroll, bool kLL, bool kNc>
-__device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
+__device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base, const uint32_t cta,
+                                      const uint32_t ncta) {
   // 1. First step of a run: publish "my inputs are in place" to every peer.
-  if (a.step == 0 && blockIdx.x == 0 && threadIdx.x < a.nsignal) {
+  if (a.step == 0 && cta == 0 && threadIdx.x < a.nsignal) {
     // Inputs were written by earlier stream work (complete at kernel
     // boundaries; peers read them through this GPU's L2): no fence needed.
     if (RS_SYNC_STRICT) FenceSys();
@@ -732,12 +735,12 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
   }
   // 2. Entry barrier: the ranks whose buffers this step touches (and whose
   //    previous-step writers) have finished the previous step.
-  RS_TRACE(3ull * a.npieces + 2ull * blockIdx.x);
+  RS_TRACE(3ull * a.npieces + 2ull * cta);
   if (threadIdx.x < a.nwait) {
     WaitAtLeast(a.inbox + a.wait_ranks[threadIdx.x], base + a.step - a.wait_lag, a.timeout_ns, a.error_flag);
   }
   __syncthreads();
-  RS_TRACE(3ull * a.npieces + 2ull * blockIdx.x + 1);
+  RS_TRACE(3ull * a.npieces + 2ull * cta + 1);
   if (a.has_nvls) FenceProxyAlias();
 
   // 3. Pieces, grid-strided; tasks are ordered by piece_begin. One-shot
@@ -751,7 +754,7 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
   };
   if constexpr (kLL) {
     uint32_t c = 0;
-    for (uint32_t p = blockIdx.x; p < a.npieces; p += gridDim.x) {
+    for (uint32_t p = cta; p < a.npieces; p += ncta) {
       while (c + 1 < a.ntasks && a.tasks[c + 1].piece_begin <= p) ++c;
       const Task& t = a.tasks[c];
       if (t.mode != kModeLL) continue;
@@ -893,15 +896,15 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
   // pieces never wait). Other phases: static grid stride.
   __shared__ uint32_t next_piece;
   auto next = [&](uint32_t p) -> uint32_t {
-    if (!a.dynamic) return p + gridDim.x;
+    if (!a.dynamic) return p + ncta;
     if (threadIdx.x == 0) next_piece = atomicAdd(a.piece_counter, 1u);
     __syncthreads();
     const uint32_t q = next_piece;
     __syncthreads();
     return q;
   };
-  for (uint32_t p = a.dynamic ? next(0) : blockIdx.x; p < a.npieces; p = next(p)) run_piece(p);
-  if (a.dynamic && threadIdx.x == 0 && atomicAdd(a.piece_counter + 1, 1u) == gridDim.x - 1) {
+  for (uint32_t p = a.dynamic ? next(0) : cta; p < a.npieces; p = next(p)) run_piece(p);
+  if (a.dynamic && threadIdx.x == 0 && atomicAdd(a.piece_counter + 1, 1u) == ncta - 1) {
     // last CTA out: reset the queue for the next launch on this rank
     atomicExch(a.piece_counter, 0u);
     atomicExch(a.piece_counter + 1, 0u);
@@ -921,11 +924,11 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base) {
       if (a.has_nvls) FenceProxyAlias();
       FenceSys();
     }
-    const bool last = gridDim.x == 1 || atomicAdd(a.arrive_counter, 1u) == gridDim.x - 1;
+    const bool last = ncta == 1 || atomicAdd(a.arrive_counter, 1u) == ncta - 1;
     if (last) {
-      if (gridDim.x > 1) atomicExch(a.arrive_counter, 0u);
+      if (ncta > 1) atomicExch(a.arrive_counter, 0u);
       if (publish) {
-        if (RS_SYNC_STRICT || gridDim.x > 1) FenceSys();  // acquire the other CTAs' releases
+        if (RS_SYNC_STRICT || ncta > 1) FenceSys();  // acquire the other CTAs' releases
         for (uint32_t q = 0; q < a.nsignal; ++q) SignalStore(a.signal_ptrs[q], base + a.step + 1);
       }
       if (last_step) {
@@ -951,7 +954,21 @@ __global__ void __launch_bounds__(512, kUnroll == 4 ? 2 : 1) StepKernel(const __
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // Run base epoch (device resident; advanced by the previous run's last step).
   const uint64_t base = a.nsignal ? *reinterpret_cast<volatile uint64_t*>(a.epoch_base) : 0;
-  Phase<DT, kUnroll, kLL, kNc>(a, base);
+  Phase<DT, kUnroll, kLL, kNc>(a, base, blockIdx.x, gridDim.x);
+}
+
+// Emulated ranks (validation on one GPU): every rank's step of one phase in
+// ONE cooperative launch, CTAs [prefix[r], prefix[r+1]) acting as rank r's
+// grid. Co-residency is what makes ranks that wait on each other safe on a
+// single GPU (separate launches are not guaranteed to run concurrently).
+template <int DT, int kUnroll, bool kLL>
+__global__ void __launch_bounds__(512, 1) EmulatedStepKernel(const __grid_constant__ EmulatedArgs e) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  uint32_t r = 0;
+  while (r + 1 < e.nranks && blockIdx.x >= e.prefix[r + 1]) ++r;
+  const StepArgs& a = e.args[r];
+  const uint64_t base = a.nsignal ? *reinterpret_cast<volatile uint64_t*>(a.epoch_base) : 0;
+  Phase<DT, kUnroll, kLL, false>(a, base, blockIdx.x - e.prefix[r], e.prefix[r + 1] - e.prefix[r]);
 }
 
 template <int U>
@@ -1018,7 +1035,50 @@ __global__ void NvlsSelfCheckKernel(char* mc, uint64_t lo, uint64_t hi) {
   asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
 
+template <int DT, int U, bool LL>
+cudaError_t LaunchEmulatedOne(const EmulatedArgs& e, int block, cudaStream_t stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(e.prefix[e.nranks]);
+  cfg.blockDim = dim3(block);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, EmulatedStepKernel<DT, U, LL>, e);
+}
+
+template <int U, bool LL>
+int EmulatedOccupancy(int dtype, int threads) {
+  int blocks = 0;
+  cudaError_t err = cudaSuccess;
+  switch (dtype) {
+    case RS_F32: err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, EmulatedStepKernel<RS_F32, U, LL>, threads, 0); break;
+    case RS_BF16: err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, EmulatedStepKernel<RS_BF16, U, LL>, threads, 0); break;
+    default: err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, EmulatedStepKernel<RS_I32, U, LL>, threads, 0); break;
+  }
+  if (err != cudaSuccess || blocks < 1) {
+    cudaGetLastError();
+    return 1;
+  }
+  return blocks;
+}
+
 }  // namespace
+
+cudaError_t LaunchEmulated(const EmulatedArgs& e, bool ll, int block, cudaStream_t stream) {
+  switch (e.args[0].dtype) {
+    case RS_F32: return ll ? LaunchEmulatedOne<RS_F32, 2, true>(e, block, stream) : LaunchEmulatedOne<RS_F32, 4, false>(e, block, stream);
+    case RS_BF16: return ll ? LaunchEmulatedOne<RS_BF16, 2, true>(e, block, stream) : LaunchEmulatedOne<RS_BF16, 4, false>(e, block, stream);
+    case RS_I32: return ll ? LaunchEmulatedOne<RS_I32, 2, true>(e, block, stream) : LaunchEmulatedOne<RS_I32, 4, false>(e, block, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+int EmulatedResidentCtas(int dtype, int threads, bool ll) {
+  return ll ? EmulatedOccupancy<2, true>(dtype, threads) : EmulatedOccupancy<4, false>(dtype, threads);
+}
 
 cudaError_t LaunchNvlsSelfCheck(char* mc, uint64_t lo, uint64_t hi, cudaStream_t stream) {
   NvlsSelfCheckKernel<<<8, 256, 0, stream>>>(mc, lo, hi);

@@ -135,6 +135,16 @@ class Context:
         return cls(h, K, {d: cuda_ordinals[d] for d in range(K)}, max_bytes)
 
     @classmethod
+    def emulated(cls, K: int, slot_rank: Sequence[int], world: int, device: int = 0, max_bytes: int = 1 << 20):
+        """Validation mode: `world` ranks emulated on one GPU (own heaps, every
+        phase one cooperative launch over all ranks) — the cross-rank kernels
+        without several GPUs (rs_ctx_create_emulated)."""
+        h = ctypes.c_void_p()
+        nat.check(nat.lib().rs_ctx_create_emulated(K, nat.int_array(slot_rank), world, device, int(max_bytes),
+                                                   ctypes.byref(h)))
+        return cls(h, K, {d: device for d in range(K)}, max_bytes)
+
+    @classmethod
     def virtual(cls, K: int, slot_rank: Sequence[int], world: int):
         """Planning-only context (no GPU): plans can be described, not run."""
         h = ctypes.c_void_p()
