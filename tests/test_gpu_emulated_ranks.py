@@ -118,3 +118,37 @@ def test_emulated_full_size_push_allreduce():
             plan.close()
     finally:
         ctx.close()
+
+
+def _dense_cases(world):
+    """Every program of the one-slot-per-rank set and of config 2 (and a
+    third of config 3) under each variant."""
+    one = ranks_worker.ONE_SLOT_SET[world]
+    cases = []
+    for variant, N, dt in (("ll", 777, numeric.BF16), ("pull", 4097, numeric.F32),
+                           ("push", (1 << 16) + 3, numeric.I32), ("reduce_push", (1 << 16) + 5, numeric.BF16)):
+        cases.append({"set": one, "K": world, "N": N, "dtype": dt, "variant": variant, "stride": 1, "runs": 1})
+    for name in ("cfg2_r1", "cfg2_r01"):
+        cases.append({"set": name, "K": 8, "N": 3001, "dtype": numeric.BF16, "variant": "pull", "stride": 1,
+                      "runs": 1})
+        cases.append({"set": name, "K": 8, "N": 1001, "dtype": numeric.I32, "variant": "ll", "stride": 1,
+                      "runs": 1})
+        cases.append({"set": name, "K": 8, "N": (1 << 16) + 3, "dtype": numeric.BF16, "variant": "push",
+                      "stride": 3, "runs": 1})
+    for name in ("cfg3_r0", "cfg3_r01", "cfg3_r12"):
+        cases.append({"set": name, "K": 8, "N": 1001, "dtype": numeric.F32, "variant": "pull", "stride": 3,
+                      "runs": 1})
+    return cases
+
+
+@pytest.mark.timeout(1800)
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_emulated_ranks_every_program(world):
+    ctxs, used = {}, {}
+    try:
+        for case in _dense_cases(world):
+            _run_case(ctxs, world, case, used)
+    finally:
+        for c in ctxs.values():
+            c.close()
+    assert all(used.get(v, 0) > 0 for v in ("ll", "pull", "push")), used
