@@ -303,6 +303,10 @@ def main():
                          "launches, which B200 does not guarantee to co-schedule (Xid 109); the N=8 path is "
                          "exercised by emulated ranks in one cooperative launch instead "
                          "(tests/test_gpu_emulated_ranks.py)")
+    ap.add_argument("--emulate-ranks", type=int, default=0,
+                    help="dry run of the N-GPU plans on ONE GPU: N ranks emulated in one process "
+                         "(rs_ctx_create_emulated, one cooperative launch per phase). Readiness of the N-rank "
+                         "plans only (no IPC, NVLS or NCCL comparator); the times are not N-GPU numbers")
     ap.add_argument("--reduce-mode", type=int, default=None, help="executor Reduce variant (0 pull, 1 push, "
                     "2 NVLS, 3 NVLS root), for A/B runs")
     args = ap.parse_args()
@@ -346,11 +350,15 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
-    slot_rank = [d * world // K_SLOTS for d in range(K_SLOTS)]
+    emu = args.emulate_ranks if not multi else 0
+    pworld = emu or world  # ranks the plans are compiled for
+    slot_rank = [d * pworld // K_SLOTS for d in range(K_SLOTS)]
 
     def make_ctx():
         if multi:
             return executor.Context.from_process_group(K_SLOTS, slot_rank, D_BYTES)
+        if emu:
+            return executor.Context.emulated(K_SLOTS, slot_rank, emu, device, D_BYTES)
         return executor.Context.local(K_SLOTS, [device] * K_SLOTS, D_BYTES)
 
     ctx = make_ctx()
@@ -472,7 +480,7 @@ def main():
     value = bus_per_step / (ms_per_step * 1e-3) / 1e9
 
     # roofline of the dominant (only) kernel: the step kernel
-    if world == 1:
+    if pworld == 1:
         alg = 0.0
         for p in plans:
             for s in range(p.program.num_steps):
@@ -493,7 +501,7 @@ def main():
                     "note": f"algorithmic bytes = sum over tasks of (sources + destinations) x range "
                             f"(minimal HBM traffic), per step {alg / 1e9:.2f} GB; peak {peak_kind}; {tnote}"}
     else:
-        if world == K_SLOTS:
+        if pworld == K_SLOTS:
             alg = sum(algorithmic_link_bytes(e["prog"], K_SLOTS, D_BYTES) for e in entries)
         else:  # several slots per GPU: the plan's own per-GPU link bytes
             alg = sum(p.step_bytes(s)[0] for p in plans for s in range(p.program.num_steps))
@@ -502,7 +510,7 @@ def main():
         try:  # committed ncu capture of the cross-GPU kernel (tools/profile_p2p.py, profiles/)
             with open(os.path.join(ROOT, "profiles", "r01_ncu_nvlink.json")) as f:
                 caps = json.load(f)
-            cap = caps.get(f"k{min(world, 4)}_push") or next(iter(caps.values()))  # large steps push
+            cap = caps.get(f"k{min(pworld, 4)}_push") or next(iter(caps.values()))  # large steps push
             traffic = cap["nvlrx_user"] + cap["nvltx_user"]
             tnote = (f"traffic = NVLink user bytes rx+tx of one profiled launch ({cap['what']}, replayed alone), "
                      f"{traffic / cap['own_share_algorithmic']:.4f} x its algorithmic bytes; link headers and flags "
@@ -539,7 +547,7 @@ def main():
     # link / HBM bytes at the measured rates; local launches ~3 us,
     # cross-GPU ~8 us incl. handshake). Configs other than this workload's are
     # timed at the end (outside every timed region) and added.
-    cal_args = dict(launch_us=3.0, link_gbs=650.0, hbm_gbs=5967.0) if world == 1 else \
+    cal_args = dict(launch_us=3.0, link_gbs=650.0, hbm_gbs=5967.0) if pworld == 1 else \
         dict(launch_us=8.0, link_gbs=650.0, hbm_gbs=5967.0)
     resc_rows = [{"instance": (args.workload, tuple(e["request"]), e["matrix"]), "index": e["index"],
                   "sim_seconds": e["prog"].seconds, "cal_us": p.predict_us(**cal_args), "measured_us": us,
@@ -639,7 +647,7 @@ def main():
         del host_in, host_out
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and pworld == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(entries, args.workload)
 
     # Config 5 over configs 1-3 (BASELINE.json): time every program of the
@@ -648,8 +656,12 @@ def main():
     rescore_configs = [args.workload] if args.workload in WORKLOADS else []
     if args.workload in WORKLOADS and not args.no_rescore_all:
         barrier()
-        extra_ctx = executor.Context.from_process_group(K_SLOTS, slot_rank, 64 << 20) if multi else \
-            executor.Context.local(K_SLOTS, [device] * K_SLOTS, 64 << 20)
+        if multi:
+            extra_ctx = executor.Context.from_process_group(K_SLOTS, slot_rank, 64 << 20)
+        elif emu:
+            extra_ctx = executor.Context.emulated(K_SLOTS, slot_rank, emu, device, 64 << 20)
+        else:
+            extra_ctx = executor.Context.local(K_SLOTS, [device] * K_SLOTS, 64 << 20)
         for name in ("config1", "config2", "config3"):
             wl = WORKLOADS[name]
             if name == args.workload or wl["bytes"] > (64 << 20):
@@ -706,7 +718,7 @@ def main():
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": bench_config(args.workload, world, len(entries)),
+            "config": bench_config(args.workload, pworld, len(entries)),
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -725,9 +737,11 @@ def main():
                              "NVLink, at N=8 one slot per GPU; value is a nccl-tests-style bus figure, so the N=1 "
                              "number measures HBM, the N>1 numbers NVLink"),
         }
-        if rpg > 1:
-            line["dry_run"] = (f"{world} ranks on {world // rpg} GPUs ({rpg} per GPU, time-sliced): readiness of the "
-                               f"N={world} launch path only; times are not {world}-GPU numbers")
+        if emu:
+            line["dry_run"] = (f"{emu} ranks emulated on one GPU (own heaps, one cooperative launch per phase): "
+                               f"readiness of the N={emu} plans only (no IPC, NVLS or NCCL comparator); times are "
+                               f"not {emu}-GPU numbers")
+            line["emulated_ranks"] = emu
         print(json.dumps(line), flush=True)
     barrier()
     for p in plans:
