@@ -23,8 +23,9 @@
  *
  * Status codes mirror absl::StatusCode: 0 OK, 3 INVALID_ARGUMENT,
  * 9 FAILED_PRECONDITION (a rule violation, same wording as
- * StepFailure::Describe, dsl.cc:135-140), 13 INTERNAL (CUDA error or a
- * device-side barrier timeout), 14 UNAVAILABLE (no GPU / extension missing).
+ * StepFailure::Describe, dsl.cc:135-140), 13 INTERNAL (CUDA error, a
+ * device-side barrier timeout, or a checked-build assertion), 14 UNAVAILABLE
+ * (no GPU / extension missing).
  * rs_last_error() returns the message of the last failing call on the thread.
  */
 #ifndef REDSYNTH_EXEC_H_
@@ -108,19 +109,26 @@ int rs_ctx_download(rs_ctx* ctx, int slot, void* host, size_t bytes, void* strea
 /* Number of ranks driven by this process and their CUDA ordinals. */
 int rs_ctx_local_ranks(rs_ctx* ctx, int* count, int* ordinals /* RS_MAX_RANKS */);
 /* Context knobs applied to plans compiled afterwards: "push_min_bytes"
- * (cross-GPU groups moving at least this many bytes use the push variant:
- * one launch, vector data crosses NVLink as stores only, chunk flags order
- * landing and reduction; -1 disables it; default 32 MiB, env
- * RS_PUSH_MIN_BYTES)
- * and "barrier_timeout_ms" (device-side spin limit, default 20 s). Scratch
+ * (cross-GPU AllReduce / balanced AllGather groups moving at least this many
+ * bytes use the push variant: one launch, vector data crosses NVLink as
+ * stores only, chunk flags order landing and reduction; -1 disables it;
+ * default 32 MiB, env RS_PUSH_MIN_BYTES), "push_wave_bytes" (push parts are
+ * landed and reduced in waves of this size; default 0 = one wave) and
+ * "barrier_timeout_ms" (device-side spin limit, default 20 s). Scratch
  * for the push variant is reserved at creation: min(K, 8) buffers per slot on
- * multi-GPU contexts (env RS_SCRATCH_REGIONS). "ll_max_bytes": a step whose
- * cross-GPU groups have one member per GPU and in which no GPU sends a peer
- * more than this many bytes runs one-shot (LL): sources are pushed as flagged
- * 16-byte packets into each receiver's LL area and every destination sums
- * locally, in group order (bit-exact like the pull path); 0 disables it
- * (default 256 KiB, env RS_LL_MAX_BYTES, capped by the per-peer area reserved
- * at creation, env RS_LL_CAPACITY, default 512 KiB). */
+ * multi-GPU contexts (env RS_SCRATCH_REGIONS). "ll_max_bytes" /
+ * "ll_total_bytes": a step whose cross-GPU groups have one member per GPU and
+ * in which no GPU sends a peer more than ll_max_bytes and no GPU sends more
+ * than ll_total_bytes in total runs one-shot (LL): sources are pushed as
+ * flagged 16-byte packets into each receiver's LL area and every destination
+ * sums locally, in group order (bit-exact like the pull path); 0 disables it
+ * (defaults 256 KiB and 16 KiB, env RS_LL_MAX_BYTES / RS_LL_TOTAL_BYTES,
+ * capped by the per-peer area reserved at creation, env RS_LL_CAPACITY,
+ * default 512 KiB). "reduce_mode" for Reduce over >= 3 GPUs: -1 auto
+ * (default: pull below "reduce_push_min_bytes" = 128 MiB, push with
+ * "reduce_wave_bytes" = 4 MiB waves above), 0 pull, 1 push, 2 NVLS (members
+ * reduce slices through the switch, store to the root; tolerance), 3 NVLS
+ * with the root reducing everything. */
 int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value);
 
 /* NVLS (NVLink SHARP): with RS_NVLS=1 at context creation the heaps are
@@ -139,8 +147,9 @@ int rs_ctx_nvls(rs_ctx* ctx, int* enabled);
  * are then collective (every rank compiles the same programs in order). */
 typedef int (*rs_exchange_fn)(const void* send, size_t bytes, void* recv, void* user);
 int rs_ctx_set_exchange(rs_ctx* ctx, rs_exchange_fn fn, void* user);
-/* Blocks until all work enqueued by this context is done; reports a
- * device-side barrier timeout (INTERNAL) if one happened. */
+/* Blocks until all work on the context's GPUs is done (device-wide: plans
+ * usually run on caller streams); reports a device-side barrier timeout
+ * (INTERNAL) once, then clears it. */
 int rs_ctx_synchronize(rs_ctx* ctx);
 
 /* ---- plans -------------------------------------------------------------- */
@@ -190,7 +199,11 @@ int rs_plan_predict_us(rs_plan* plan, double launch_us, double link_gbs, double 
 /* Tuning knobs (0 = default): CTAs per launch cap and threads per CTA. */
 int rs_plan_set_launch(rs_plan* plan, int max_ctas, int threads);
 /* Named knobs: "unroll" (4|8 vectors in flight per thread per source),
- * "threads" (per CTA), "max_ctas" (per launch, 0 = resident capacity). */
+ * "threads" (per CTA), "max_ctas" (per launch, 0 = resident capacity),
+ * "wide_loads" (cross-GPU sums load every source before adding; default 1),
+ * "dynamic_pieces" (push phases take pieces from an atomic queue; default 1),
+ * "pdl" (programmatic dependent launch; default 0, measured neutral),
+ * "local_wide" (one-GPU sums load every source first; default 0). */
 int rs_plan_set_option(rs_plan* plan, const char* key, long long value);
 
 /* JSON dump of the compiled plan: per step, per rank, the entry-barrier
