@@ -489,7 +489,7 @@ def main():
         achieved = alg / (ms_per_step * 1e-3) / 1e9
         traffic, tnote = None, "no ncu capture found"
         try:  # committed ncu --set full capture of the same kernel (profiles/)
-            with open(os.path.join(ROOT, "profiles", "r01b_ncu_local.json")) as f:
+            with open(os.path.join(ROOT, "profiles", "r02_ncu_local.json")) as f:
                 cap = json.load(f)["launches"][0]
             traffic = cap["dram_bytes"]
             tnote = (f"traffic = dram read+write bytes of one profiled launch ({cap['what']}), "
