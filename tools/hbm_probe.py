@@ -32,9 +32,22 @@ def main():
             out = max(out, nbytes / (a.elapsed_time(b) * 1e-3) / 1e9)
         return round(out, 1)
 
+    import ctypes
+    rt = None
+    for name in ("libcudart.so", "libcudart.so.12"):
+        try:
+            rt = ctypes.CDLL(name)
+            break
+        except OSError:
+            continue
+    memset = None
+    if rt is not None:
+        rt.cudaMemsetAsync.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t, ctypes.c_void_p]
+        memset = lambda: rt.cudaMemsetAsync(ctypes.c_void_p(y.data_ptr()), 0, 2 * n, ctypes.c_void_p(s.cuda_stream))
     res = {
         "read_only_sum_GBps": best(lambda: x.sum(dtype=torch.float32), 2 * n),
         "write_only_fill_GBps": best(lambda: y.fill_(1.0), 2 * n),
+        "write_only_memset_GBps": best(memset, 2 * n) if memset else None,
         "copy_1r1w_GBps": best(lambda: y.copy_(x), 4 * n),
     }
     print(json.dumps(res), flush=True)
