@@ -9,3 +9,4 @@ import json,sys
 for l in open(sys.argv[1]):
     if l.startswith('{'):
         d=json.loads(l); print(sys.argv[1], d['value'], d['ms_per_step'], (d.get('roofline') or {}).get('frac'), (d.get('e2e') or {}).get('value'), d.get('clocks'), (d.get('cpu_baseline') or {}).get('value'))" gpurun_out/$f.log; done
+python tools/hbm_probe.py > gpurun_out/r02_hbm_probe.txt 2>&1; cat gpurun_out/r02_hbm_probe.txt
