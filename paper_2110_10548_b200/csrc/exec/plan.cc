@@ -91,9 +91,14 @@ uint64_t TotalBytes(const std::vector<Range>& ranges) {
   return t;
 }
 
+// Vector bodies are kVecAlign-aligned (32 B: the one-GPU kernel moves
+// 256-bit vectors); owner cuts sit on such offsets, shorter edges become
+// scalar tasks.
+constexpr uint64_t kVecAlign = 32;
+
 // Splits the concatenation of `ranges` into k consecutive parts of nearly
-// equal size whose cut points sit on 16-byte buffer offsets (or on range
-// starts), so owners' vector work stays aligned.
+// equal size whose cut points sit on kVecAlign-byte buffer offsets (or on
+// range starts), so owners' vector work stays aligned.
 std::vector<std::vector<Range>> SplitEven(const std::vector<Range>& ranges, int k) {
   std::vector<std::vector<Range>> parts(k);
   if (ranges.empty() || k <= 0) return parts;
@@ -104,7 +109,7 @@ std::vector<std::vector<Range>> SplitEven(const std::vector<Range>& ranges, int 
       const uint64_t len = r.hi - r.lo;
       if (c < base + len || (&r == &ranges.back())) {
         const uint64_t b = std::min(r.lo + (c - base), r.hi);
-        uint64_t a = b & ~uint64_t{15};
+        uint64_t a = b & ~(kVecAlign - 1);
         if (a < r.lo) a = r.lo;
         return base + (a - r.lo);
       }
@@ -701,10 +706,10 @@ void Lay(RankStep& rs, const ProtoTask& t, uint32_t piece_bytes, uint64_t flag_c
     rs.npieces += vec ? static_cast<uint32_t>((hi - lo + piece_bytes - 1) / piece_bytes) : 1u;
     rs.tasks.push_back(task);
   };
-  const uint64_t a = (t.range.lo + 15) & ~uint64_t{15};
-  const uint64_t b = t.range.hi & ~uint64_t{15};
+  const uint64_t a = (t.range.lo + kVecAlign - 1) & ~(kVecAlign - 1);
+  const uint64_t b = t.range.hi & ~(kVecAlign - 1);
   if (a >= b) {
-    // No aligned body: at most 30 bytes, two scalar tasks keep each < 16 B.
+    // No aligned body: at most 62 bytes, two scalar tasks keep each < 32 B.
     const uint64_t mid = std::min(std::max(a, t.range.lo), t.range.hi);
     push(t.range.lo, mid, false);
     push(mid, t.range.hi, false);
@@ -945,6 +950,7 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
   if (const char* v = std::getenv("RS_DYNAMIC_PIECES")) plan->dynamic_pieces = std::atoi(v) != 0;
   if (const char* v = std::getenv("RS_PDL")) plan->pdl = std::atoi(v) != 0;
   if (const char* v = std::getenv("RS_LOCAL_WIDE")) plan->local_wide = std::atoi(v) != 0;
+  if (const char* v = std::getenv("RS_VEC256")) plan->vec256 = std::atoi(v);
   {
     const uint64_t rp = ctx->recv_piece_bytes;
     plan->recv_piece = static_cast<uint32_t>(rp >= 16 && rp % 16 == 0 && ctx->flag_chunk % rp == 0 ? rp : ctx->flag_chunk);

@@ -78,6 +78,7 @@ void BuildLaunches(Plan* plan) {
       a.wide_loads = plan->wide_loads ? 1u : 0u;
       a.pdl = plan->pdl ? 1u : 0u;
       a.local_wide = plan->local_wide ? 1u : 0u;
+      a.vec256 = static_cast<uint32_t>(plan->vec256);
       a.slot_limit = ctx->slot_stride;
       a.signal_done = rsx.signal_done ? 1u : 0u;
       a.wait_lag = static_cast<uint32_t>(plan->phase_lag[ph]);

@@ -262,6 +262,108 @@ __device__ __forceinline__ void VectorChunk(const Task& t, void* const* ptrs, ui
   }
 }
 
+// 256-bit streaming load / store (sm_100): 32 bytes per thread per
+// instruction. Single-rank (local) launches only: non-coherent loads.
+struct Vec32 {
+  uint4 lo, hi;
+};
+
+__device__ __forceinline__ Vec32 LoadStream32(const void* p) {
+  Vec32 v;
+  asm volatile("ld.global.nc" RS_LOAD_QUAL ".v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v.lo.x), "=r"(v.lo.y), "=r"(v.lo.z), "=r"(v.lo.w), "=r"(v.hi.x), "=r"(v.hi.y), "=r"(v.hi.z),
+                 "=r"(v.hi.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void Store32(void* p, const Vec32& v) {
+  asm volatile("st.global" RS_STORE_QUAL ".v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v.lo.x),
+               "r"(v.lo.y), "r"(v.lo.z), "r"(v.lo.w), "r"(v.hi.x), "r"(v.hi.y), "r"(v.hi.z), "r"(v.hi.w)
+               : "memory");
+}
+
+// One-GPU copy chunk (a single source: the AllGather / Broadcast tasks, the
+// write-heavy steps) with 256-bit vectors: thread t handles 32-byte vectors
+// begin + (u * blockDim + t) * 32, u < kU. Measured on a 1-read / 3-write
+// copy at 148 x 512 threads: 6.16 TB/s vs 4.83 with 128-bit vectors
+// (tools/hbm_write_probe.cu, profiles/r02_hbm_write_probe.txt). Sums keep
+// the 128-bit path (their f32 accumulators would not fit beside 256-bit
+// batches; they are read-heavy and already near the HBM rate).
+template <int kU>
+__device__ __forceinline__ void CopyChunk32(const Task& t, void* const* ptrs, uint64_t begin, uint64_t end) {
+  uint64_t off[kU];
+  bool ok[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    off[u] = begin + (static_cast<uint64_t>(u) * blockDim.x + threadIdx.x) * 32u;
+    ok[u] = off[u] < end;
+  }
+  void* const* src = ptrs + t.ptr_begin;
+  void* const* dst = src + t.nsrc;
+  Vec32 raw[kU];
+  const char* s0 = static_cast<const char*>(src[0]);
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    raw[u] = Vec32{make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};  // defined on every path (no spills)
+    if (ok[u]) raw[u] = LoadStream32(s0 + off[u]);
+  }
+  for (int j = 0; j < t.ndst; ++j) {
+    char* d = static_cast<char*>(dst[j]);
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (ok[u]) Store32(d + off[u], raw[u]);
+  }
+}
+
+// One-GPU sum chunk with 256-bit vectors (A/B: vec256 = 2): as
+// VectorChunk<DT, 2 kU> but 32 bytes per memory instruction.
+template <int DT, int kU>
+__device__ __forceinline__ void SumChunk32(const Task& t, void* const* ptrs, uint64_t begin, uint64_t end) {
+  using Acc = typename AccOf<DT>::T;
+  uint64_t off[kU];
+  bool ok[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    off[u] = begin + (static_cast<uint64_t>(u) * blockDim.x + threadIdx.x) * 32u;
+    ok[u] = off[u] < end;
+  }
+  void* const* src = ptrs + t.ptr_begin;
+  void* const* dst = src + t.nsrc;
+  Vec32 raw[kU];
+  const char* s0 = static_cast<const char*>(src[0]);
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    raw[u] = Vec32{make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+    if (ok[u]) raw[u] = LoadStream32(s0 + off[u]);
+  }
+  Acc acc[2 * kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    acc[2 * u].Init(raw[u].lo);
+    acc[2 * u + 1].Init(raw[u].hi);
+  }
+  for (int i = 1; i < t.nsrc; ++i) {
+    const char* si = static_cast<const char*>(src[i]);
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (ok[u]) raw[u] = LoadStream32(si + off[u]);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      acc[2 * u].Add(raw[u].lo);
+      acc[2 * u + 1].Add(raw[u].hi);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kU; ++u) raw[u] = Vec32{acc[2 * u].Pack(), acc[2 * u + 1].Pack()};
+  for (int j = 0; j < t.ndst; ++j) {
+    char* d = static_cast<char*>(dst[j]);
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (ok[u]) Store32(d + off[u], raw[u]);
+  }
+}
+
 // Cross-GPU pull chunk with every source's loads in flight at once: all
 // nsrc (<= kS) sources' kU vectors are loaded before the first add, so a
 // chunk costs one round trip instead of nsrc serialized ones; the sum is
@@ -866,19 +968,17 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base, co
         }
       }
       if constexpr (kNc && kUnroll == 8) {
-        // one GPU: every source's loads in flight at once (A/B: RS_LOCAL_WIDE)
-        if (a.local_wide && t.nsrc >= 2 && t.nsrc <= 4) {
-          constexpr uint64_t kW = 4;
-          const uint64_t wchunk = static_cast<uint64_t>(blockDim.x) * kW * 16u;
-          for (uint64_t c = begin; c < end; c += wchunk)
-            VectorChunkWide<DT, 4, kW, false, true>(t, a.ptrs, c, min(end, c + wchunk));
-          done = true;
-        } else if (a.local_wide && t.nsrc > 4 && t.nsrc <= 8) {
-          constexpr uint64_t kW = 2;
-          const uint64_t wchunk = static_cast<uint64_t>(blockDim.x) * kW * 16u;
-          for (uint64_t c = begin; c < end; c += wchunk)
-            VectorChunkWide<DT, 8, kW, false, true>(t, a.ptrs, c, min(end, c + wchunk));
-          done = true;
+        // one GPU, single-source copy with a 32-byte aligned body: 256-bit
+        // vectors (kUnroll / 2 per thread, the same bytes in flight)
+        if (!done && a.vec256 && ((t.lo | t.hi) & 31) == 0) {
+          if (t.nsrc == 1) {
+            for (uint64_t c = begin; c < end; c += chunk) CopyChunk32<kUnroll / 2>(t, a.ptrs, c, min(end, c + chunk));
+            done = true;
+          } else if (a.vec256 >= 2) {
+            for (uint64_t c = begin; c < end; c += chunk)
+              SumChunk32<DT, kUnroll / 2>(t, a.ptrs, c, min(end, c + chunk));
+            done = true;
+          }
         }
       }
       if (!done) {

@@ -121,7 +121,7 @@ def _simulate_tasks(tasks, every, bufs, mem, scratch, es, view, dtype):
             elif t["vec"]:  # (push landing / reducing bodies are 16-byte aligned too)
                 assert t["lo"] % 16 == 0 and t["hi"] % 16 == 0
             else:
-                assert t["hi"] - t["lo"] < 16
+                assert t["hi"] - t["lo"] < 32
             lo, hi = t["lo"] // es, t["hi"] // es
             srcs = [src_mem(s, rg).view(view)[lo:hi] for s, rg in zip(t["src"], t["src_region"])]
             if len(srcs) == 1:

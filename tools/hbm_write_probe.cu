@@ -21,6 +21,66 @@
 
 enum Store { kPlain = 0, kNoAlloc = 1, kCs = 2, kEvictFirst = 3, kWb = 4 };
 
+// 256-bit (sm_100) load / store: 32 bytes per thread per instruction.
+struct V8 {
+  uint32_t r[8];
+};
+template <int S>
+__device__ __forceinline__ void St8(void* p, const V8& v) {
+  if constexpr (S == kEvictFirst) {
+    asm volatile("st.global.L1::no_allocate.L2::evict_first.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+                 "r"(v.r[0]), "r"(v.r[1]), "r"(v.r[2]), "r"(v.r[3]), "r"(v.r[4]), "r"(v.r[5]), "r"(v.r[6]),
+                 "r"(v.r[7]) : "memory");
+  } else {
+    asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.r[0]),
+                 "r"(v.r[1]), "r"(v.r[2]), "r"(v.r[3]), "r"(v.r[4]), "r"(v.r[5]), "r"(v.r[6]), "r"(v.r[7]) : "memory");
+  }
+}
+__device__ __forceinline__ V8 Ld8(const void* p) {
+  V8 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v.r[0]), "=r"(v.r[1]), "=r"(v.r[2]), "=r"(v.r[3]), "=r"(v.r[4]), "=r"(v.r[5]), "=r"(v.r[6]),
+                 "=r"(v.r[7])
+               : "l"(p));
+  return v;
+}
+
+template <int S, int U>
+__global__ void fill8_kernel(V8* dst, size_t n, uint32_t seed) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x * U;
+  for (size_t base = static_cast<size_t>(blockIdx.x) * blockDim.x * U + threadIdx.x; base < n; base += stride) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const size_t i = base + static_cast<size_t>(u) * blockDim.x;
+      V8 v;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v.r[k] = seed ^ static_cast<uint32_t>(i * 8 + k);
+      if (i < n) St8<S>(dst + i, v);
+    }
+  }
+}
+
+template <int S, int U, int K>
+__global__ void bcast8_kernel(V8* const* dst, const V8* src, size_t n) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x * U;
+  for (size_t base = static_cast<size_t>(blockIdx.x) * blockDim.x * U + threadIdx.x; base < n; base += stride) {
+    V8 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const size_t i = base + static_cast<size_t>(u) * blockDim.x;
+      if (i < n) v[u] = Ld8(src + i);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t i = base + static_cast<size_t>(u) * blockDim.x;
+        if (i < n) St8<S>(dst[k] + i, v[u]);
+      }
+    }
+  }
+}
+
 template <int S>
 __device__ __forceinline__ void St(void* p, const uint4& v) {
   if constexpr (S == kPlain) {
@@ -32,7 +92,7 @@ __device__ __forceinline__ void St(void* p, const uint4& v) {
     asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
   } else if constexpr (S == kEvictFirst) {
     asm volatile("st.global.L1::no_allocate.L2::evict_first.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
-                 "r"(v.z), "r"(v.w) : "memory");
+                 "r"(v.z), "r"(v.w) : "memory");  // (ptxas: evict_first needs 256-bit stores; kept for kWide256)
   } else {
     asm volatile("st.global.wb.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
   }
@@ -129,7 +189,28 @@ int main(int argc, char** argv) {
   RunFill<kPlain, 4>("plain", buf[7], n, sms * 4, 512);
   RunFill<kNoAlloc, 4>("L1::no_allocate", buf[7], n, sms * 4, 512);
   RunFill<kCs, 4>("cs", buf[7], n, sms * 4, 512);
-  RunFill<kEvictFirst, 4>("L2::evict_first", buf[7], n, sms * 4, 512);
+  {
+    const size_t n8 = bytes / 32;
+    V8* d8 = reinterpret_cast<V8*>(buf[7]);
+    double t = Time([&] { fill8_kernel<kNoAlloc, 4><<<sms * 4, 512>>>(d8, n8, 7u); }, 10);
+    std::printf("{\"probe\": \"fill 256-bit no_allocate U=4\", \"GBps\": %.1f}\n", bytes / t / 1e9);
+    t = Time([&] { fill8_kernel<kEvictFirst, 4><<<sms * 4, 512>>>(d8, n8, 7u); }, 10);
+    std::printf("{\"probe\": \"fill 256-bit evict_first U=4\", \"GBps\": %.1f}\n", bytes / t / 1e9);
+    t = Time([&] { fill8_kernel<kNoAlloc, 2><<<sms * 8, 256>>>(d8, n8, 7u); }, 10);
+    std::printf("{\"probe\": \"fill 256-bit no_allocate U=2 256thr\", \"GBps\": %.1f}\n", bytes / t / 1e9);
+    V8* const* dp8 = reinterpret_cast<V8* const*>(dptrs);
+    const V8* s8 = reinterpret_cast<const V8*>(buf[0]);
+    t = Time([&] { bcast8_kernel<kNoAlloc, 4, 3><<<sms, 512>>>(dp8, s8, n8); }, 10);
+    std::printf("{\"probe\": \"1r3w 256-bit no_allocate U=4\", \"GBps\": %.1f}\n", bytes * 4.0 / t / 1e9);
+    t = Time([&] { bcast8_kernel<kEvictFirst, 4, 3><<<sms, 512>>>(dp8, s8, n8); }, 10);
+    std::printf("{\"probe\": \"1r3w 256-bit evict_first U=4\", \"GBps\": %.1f}\n", bytes * 4.0 / t / 1e9);
+    t = Time([&] { bcast8_kernel<kNoAlloc, 2, 3><<<sms * 2, 512>>>(dp8, s8, n8); }, 10);
+    std::printf("{\"probe\": \"1r3w 256-bit no_allocate U=2 2cta\", \"GBps\": %.1f}\n", bytes * 4.0 / t / 1e9);
+    t = Time([&] { bcast8_kernel<kNoAlloc, 4, 7><<<sms, 512>>>(dp8, s8, n8); }, 10);
+    std::printf("{\"probe\": \"1r7w 256-bit no_allocate U=4\", \"GBps\": %.1f}\n", bytes * 8.0 / t / 1e9);
+    t = Time([&] { bcast8_kernel<kNoAlloc, 4, 1><<<sms, 512>>>(dp8, s8, n8); }, 10);
+    std::printf("{\"probe\": \"1r1w 256-bit no_allocate U=4\", \"GBps\": %.1f}\n", bytes * 2.0 / t / 1e9);
+  }
   RunFill<kNoAlloc, 8>("L1::no_allocate", buf[7], n, sms * 2, 512);
   RunFill<kNoAlloc, 4>("L1::no_allocate", buf[7], n, sms * 16, 256);
   RunFill<kNoAlloc, 1>("L1::no_allocate", buf[7], n, sms * 32, 256);
@@ -138,10 +219,8 @@ int main(int argc, char** argv) {
   RunBcast<kNoAlloc, 4, 3>("L1::no_allocate", dptrs, buf[0], n, sms * 2, 512);
   RunBcast<kNoAlloc, 2, 3>("L1::no_allocate", dptrs, buf[0], n, sms * 4, 512);
   RunBcast<kCs, 8, 3>("cs", dptrs, buf[0], n, sms, 512);
-  RunBcast<kEvictFirst, 8, 3>("L2::evict_first", dptrs, buf[0], n, sms, 512);
   RunBcast<kPlain, 8, 3>("plain", dptrs, buf[0], n, sms, 512);
   RunBcast<kNoAlloc, 8, 7>("L1::no_allocate", dptrs, buf[0], n, sms, 512);
   RunBcast<kNoAlloc, 2, 7>("L1::no_allocate", dptrs, buf[0], n, sms * 4, 512);
-  RunBcast<kEvictFirst, 8, 7>("L2::evict_first", dptrs, buf[0], n, sms, 512);
   return 0;
 }
