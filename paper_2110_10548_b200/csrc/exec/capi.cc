@@ -331,10 +331,12 @@ int rs_plan_set_option(rs_plan* plan, const char* key, long long value) {
     plan->impl->pdl = value != 0;
   } else if (k == "local_wide") {
     plan->impl->local_wide = value != 0;
+  } else if (k == "remote256") {
+    plan->impl->remote256 = value != 0;
   } else if (k == "vec256") {
     plan->impl->vec256 = static_cast<int>(value);
   } else {
-    return Bad("unknown option (unroll | threads | max_ctas | wide_loads | dynamic_pieces | pdl | local_wide | vec256)");
+    return Bad("unknown option (unroll | threads | max_ctas | wide_loads | dynamic_pieces | pdl | local_wide | vec256 | remote256)");
   }
   plan->impl->ctas_per_sm = 0;
   return RS_OK;

@@ -86,6 +86,7 @@ struct StepArgs {
   uint32_t pdl;               // launched with programmatic stream serialization
   uint32_t local_wide;        // one-GPU sums load every source before adding
   uint32_t vec256;            // one-GPU bodies move 256-bit vectors
+  uint32_t remote256;         // cross-GPU sums move 256-bit vectors
   uint64_t slot_limit;        // bytes addressable per slot region (checked builds assert task ranges)
   uint32_t solo;              // profiling builds only (RS_PROFILING_AIDS): skip every cross-GPU wait
   uint64_t* trace;            // profiling builds only: %globaltimer stamps per piece (RS_TRACE_PTR)

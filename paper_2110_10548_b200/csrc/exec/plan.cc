@@ -951,6 +951,7 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
   if (const char* v = std::getenv("RS_PDL")) plan->pdl = std::atoi(v) != 0;
   if (const char* v = std::getenv("RS_LOCAL_WIDE")) plan->local_wide = std::atoi(v) != 0;
   if (const char* v = std::getenv("RS_VEC256")) plan->vec256 = std::atoi(v);
+  if (const char* v = std::getenv("RS_REMOTE256")) plan->remote256 = std::atoi(v) != 0;
   {
     const uint64_t rp = ctx->recv_piece_bytes;
     plan->recv_piece = static_cast<uint32_t>(rp >= 16 && rp % 16 == 0 && ctx->flag_chunk % rp == 0 ? rp : ctx->flag_chunk);

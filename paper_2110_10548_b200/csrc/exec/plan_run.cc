@@ -79,6 +79,7 @@ void BuildLaunches(Plan* plan) {
       a.pdl = plan->pdl ? 1u : 0u;
       a.local_wide = plan->local_wide ? 1u : 0u;
       a.vec256 = static_cast<uint32_t>(plan->vec256);
+      a.remote256 = plan->remote256 ? 1u : 0u;
       a.slot_limit = ctx->slot_stride;
       a.signal_done = rsx.signal_done ? 1u : 0u;
       a.wait_lag = static_cast<uint32_t>(plan->phase_lag[ph]);

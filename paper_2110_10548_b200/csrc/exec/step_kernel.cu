@@ -316,6 +316,46 @@ __device__ __forceinline__ void CopyChunk32(const Task& t, void* const* ptrs, ui
   }
 }
 
+// Weak (coherent-after-acquire) 256-bit load for cross-GPU sources.
+__device__ __forceinline__ Vec32 LoadWeak32(const void* p) {
+  Vec32 v;
+  asm volatile("ld.global" RS_LOAD_QUAL ".v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v.lo.x), "=r"(v.lo.y), "=r"(v.lo.z), "=r"(v.lo.w), "=r"(v.hi.x), "=r"(v.hi.y), "=r"(v.hi.z),
+                 "=r"(v.hi.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+
+// Cross-GPU sum with 256-bit vectors and every source in flight (A/B:
+// remote256): one 32-byte vector per thread per source.
+template <int DT, int kS>
+__device__ __forceinline__ void WideChunk32(const Task& t, void* const* ptrs, uint64_t begin, uint64_t end) {
+  using Acc = typename AccOf<DT>::T;
+  const uint64_t off = begin + static_cast<uint64_t>(threadIdx.x) * 32u;
+  if (off >= end) return;
+  void* const* src = ptrs + t.ptr_begin;
+  void* const* dst = src + t.nsrc;
+  Vec32 raw[kS];
+#pragma unroll
+  for (int i = 0; i < kS; ++i) {
+    raw[i] = Vec32{make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+    if (i < t.nsrc) raw[i] = LoadWeak32(static_cast<const char*>(src[i]) + off);
+  }
+  Acc lo, hi;
+  lo.Init(raw[0].lo);
+  hi.Init(raw[0].hi);
+#pragma unroll
+  for (int i = 1; i < kS; ++i) {
+    if (i < t.nsrc) {
+      lo.Add(raw[i].lo);
+      hi.Add(raw[i].hi);
+    }
+  }
+  const Vec32 out{lo.Pack(), hi.Pack()};
+  for (int j = 0; j < t.ndst; ++j) Store32(static_cast<char*>(dst[j]) + off, out);
+}
+
 // One-GPU sum chunk with 256-bit vectors (A/B: vec256 = 2): as
 // VectorChunk<DT, 2 kU> but 32 bytes per memory instruction.
 template <int DT, int kU>
@@ -952,6 +992,11 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base, co
         }
       }
       if constexpr (!kNc) {
+        if (!done && a.remote256 && t.nsrc >= 2 && t.nsrc <= 4 && ((t.lo | t.hi) & 31) == 0) {
+          const uint64_t wchunk = static_cast<uint64_t>(blockDim.x) * 32u;
+          for (uint64_t c = begin; c < end; c += wchunk) WideChunk32<DT, 4>(t, a.ptrs, c, min(end, c + wchunk));
+          done = true;
+        }
         if (!done && a.wide_loads && t.nsrc >= 2 && t.nsrc <= 8) {
           // cross-GPU sums: every source in flight at once (see VectorChunkWide)
           if (t.nsrc <= 4) {
