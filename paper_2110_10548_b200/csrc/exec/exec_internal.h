@@ -226,7 +226,10 @@ class Plan {
   uint32_t recv_piece = kFlagChunk;  // effective push reducing piece of this plan
   bool dynamic_pieces = true;
   bool pdl = false;  // programmatic dependent launch of every step (option "pdl", env RS_PDL): measured neutral
-  bool remote256 = false;  // cross-GPU pull sums with 256-bit vectors (option "remote256", env RS_REMOTE256)
+  // cross-GPU pull sums, push landing copies and push reductions with 256-bit
+  // vectors (option "remote256", env RS_REMOTE256): K=4 pull 16-256 MiB
+  // AllReduce -2.5 %, ReduceScatter -4 %, Reduce -3 % (profiles/r02_remote256_ab.txt)
+  bool remote256 = true;
   int vec256 = 2;  // one-GPU 256-bit vectors: 1 copies, 2 copies and sums (option "vec256", env RS_VEC256)
   bool local_wide = false;  // one-GPU sums: all sources in flight (option "local_wide", env RS_LOCAL_WIDE)  // push phases take pieces from an atomic queue (option / env RS_DYNAMIC_PIECES)
   bool wide_loads = true;  // cross-GPU pull sums: all sources in flight (option "wide_loads", env RS_WIDE_LOADS)

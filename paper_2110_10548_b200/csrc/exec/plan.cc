@@ -178,7 +178,7 @@ struct Compiler {
     const uint64_t w = wave_bytes == ~0ull ? ctx->push_wave_bytes : wave_bytes;
     if (w == 0 || r.hi - r.lo <= w) return {r};
     std::vector<Range> out;
-    const uint64_t a = (r.lo + 15) & ~uint64_t{15};
+    const uint64_t a = (r.lo + kVecAlign - 1) & ~(kVecAlign - 1);
     uint64_t lo = r.lo;
     for (uint64_t cut = a + w; cut < r.hi; cut += w) {
       out.push_back(Range{lo, cut});
@@ -579,8 +579,8 @@ Ref NullRef() { return Ref{-1, kNullRegion}; }
 // task is its vector body (chunk flags appended to the pointer table) plus
 // edges that pull like the default variant.
 void LayFlagged(RankStep& rs, const ProtoTask& t, uint64_t chunk, uint64_t recv_piece) {
-  const uint64_t a = (t.range.lo + 15) & ~uint64_t{15};
-  const uint64_t b = t.range.hi & ~uint64_t{15};
+  const uint64_t a = (t.range.lo + kVecAlign - 1) & ~(kVecAlign - 1);
+  const uint64_t b = t.range.hi & ~(kVecAlign - 1);
   auto scalar = [&](uint64_t lo, uint64_t hi) {
     if (hi <= lo || t.edge_dst.empty()) return;
     Task task{};
@@ -614,7 +614,7 @@ void LayFlagged(RankStep& rs, const ProtoTask& t, uint64_t chunk, uint64_t recv_
     rs.tasks.push_back(task);
     return;
   }
-  if (!body) {  // < 32 bytes: everything pulls
+  if (!body) {  // < 64 bytes: everything pulls
     const uint64_t mid = std::min(std::max(a, t.range.lo), t.range.hi);
     scalar(t.range.lo, mid);
     scalar(mid, t.range.hi);

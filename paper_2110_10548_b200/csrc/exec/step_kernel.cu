@@ -327,9 +327,45 @@ __device__ __forceinline__ Vec32 LoadWeak32(const void* p) {
   return v;
 }
 
-// Cross-GPU sum with 256-bit vectors and every source in flight (A/B:
-// remote256): one 32-byte vector per thread per source.
-template <int DT, int kS>
+__device__ __forceinline__ Vec32 LoadCoherent32(const void* p) {
+  Vec32 v;
+  asm volatile("ld.global.cg.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v.lo.x), "=r"(v.lo.y), "=r"(v.lo.z), "=r"(v.lo.w), "=r"(v.hi.x), "=r"(v.hi.y), "=r"(v.hi.z),
+                 "=r"(v.hi.w)
+               : "l"(p));
+  return v;
+}
+
+// Cross-GPU copy with 256-bit vectors (push landing pieces): kU 32-byte
+// vectors per thread, weak loads.
+template <int kU>
+__device__ __forceinline__ void RemoteCopyChunk32(const Task& t, void* const* ptrs, uint64_t begin, uint64_t end) {
+  uint64_t off[kU];
+  bool ok[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    off[u] = begin + (static_cast<uint64_t>(u) * blockDim.x + threadIdx.x) * 32u;
+    ok[u] = off[u] < end;
+  }
+  void* const* src = ptrs + t.ptr_begin;
+  void* const* dst = src + t.nsrc;
+  Vec32 raw[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    raw[u] = Vec32{make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+    if (ok[u]) raw[u] = LoadWeak32(static_cast<const char*>(src[0]) + off[u]);
+  }
+  for (int j = 0; j < t.ndst; ++j) {
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (ok[u]) Store32(static_cast<char*>(dst[j]) + off[u], raw[u]);
+  }
+}
+
+// Cross-GPU sum with 256-bit vectors and every source in flight (option
+// remote256, default on): one 32-byte vector per thread per source; kCoherent
+// for push reductions over landed scratch (written during this kernel).
+template <int DT, int kS, bool kCoherent = false>
 __device__ __forceinline__ void WideChunk32(const Task& t, void* const* ptrs, uint64_t begin, uint64_t end) {
   using Acc = typename AccOf<DT>::T;
   const uint64_t off = begin + static_cast<uint64_t>(threadIdx.x) * 32u;
@@ -340,7 +376,9 @@ __device__ __forceinline__ void WideChunk32(const Task& t, void* const* ptrs, ui
 #pragma unroll
   for (int i = 0; i < kS; ++i) {
     raw[i] = Vec32{make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-    if (i < t.nsrc) raw[i] = LoadWeak32(static_cast<const char*>(src[i]) + off);
+    if (i < t.nsrc)
+      raw[i] = kCoherent ? LoadCoherent32(static_cast<const char*>(src[i]) + off)
+                         : LoadWeak32(static_cast<const char*>(src[i]) + off);
   }
   Acc lo, hi;
   lo.Init(raw[0].lo);
@@ -948,7 +986,10 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base, co
         }
         __syncthreads();
         RS_TRACE(3ull * p + 1);
-        if (a.wide_loads && t.nsrc >= 2 && t.nsrc <= 4) {
+        if (a.remote256 && t.nsrc >= 2 && t.nsrc <= 4 && ((t.lo | t.hi) & 31) == 0) {
+          const uint64_t wchunk = static_cast<uint64_t>(blockDim.x) * 32u;
+          for (uint64_t c = begin; c < end; c += wchunk) WideChunk32<DT, 4, true>(t, a.ptrs, c, min(end, c + wchunk));
+        } else if (a.wide_loads && t.nsrc >= 2 && t.nsrc <= 4) {
           constexpr uint64_t kW = 2;
           const uint64_t wchunk = static_cast<uint64_t>(blockDim.x) * kW * 16u;
           for (uint64_t c = begin; c < end; c += wchunk)
@@ -964,8 +1005,12 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base, co
       } else {
         const uint64_t begin = t.lo + static_cast<uint64_t>(k) * a.flag_chunk;
         const uint64_t end = min(t.hi, begin + a.flag_chunk);
-        for (uint64_t c = begin; c < end; c += chunk)
-          VectorChunk<DT, kUnroll, kNc>(t, a.ptrs, c, min(end, c + chunk));
+        if (a.remote256 && t.nsrc == 1 && ((t.lo | t.hi) & 31) == 0) {
+          for (uint64_t c = begin; c < end; c += chunk) RemoteCopyChunk32<kUnroll / 2>(t, a.ptrs, c, min(end, c + chunk));
+        } else {
+          for (uint64_t c = begin; c < end; c += chunk)
+            VectorChunk<DT, kUnroll, kNc>(t, a.ptrs, c, min(end, c + chunk));
+        }
         __syncthreads();
         RS_TRACE(3ull * p + 1);
         if (threadIdx.x == 0) {
