@@ -205,6 +205,7 @@ struct RankStep {
   std::vector<Ref> ptr_refs;  // pointer-table entries
   uint32_t npieces = 0;
   uint32_t piece_bytes = kPieceBytes;  // 4 KiB .. 64 KiB, sized to fill the GPU
+  uint32_t recv_piece = kFlagChunk;    // push reducing piece (divides flag_chunk)
   uint32_t max_grid = 0;      // 0 = resident capacity (one-shot phases: a few CTAs)
   int remote_peers = 0;       // distinct peer GPUs the tasks address
   std::vector<uint8_t> wait;  // ranks to wait for before the phase

@@ -1037,11 +1037,17 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
       uint32_t pb = 4u << 10;
       while (pb < kPieceBytes && rank_bytes[r] / pb > 2 * sms) pb <<= 1;
       plan->phases.back()[r].piece_bytes = pb;
+      // Push reductions: 64 KiB pieces keep every CTA busy when results fan
+      // out to n members (AllReduce, AllGather); a Reduce's owners store one
+      // result each and run best on whole chunks (K=4 1 GiB 2,186 -> 1,812 us,
+      // profiles/r02_reduce_variants_k4.txt).
+      plan->phases.back()[r].recv_piece = step.op == Collective::kReduce ? static_cast<uint32_t>(ctx->flag_chunk)
+                                                                         : plan->recv_piece;
     }
     for (const ProtoTask& t : list) {
       AddTraffic(plan->phases.back(), *ctx, t);
       RankStep& rs = plan->phases.back()[ctx->slot_rank[t.owner]];
-      Lay(rs, t, rs.piece_bytes, ctx->flag_chunk, plan->recv_piece);
+      Lay(rs, t, rs.piece_bytes, ctx->flag_chunk, rs.recv_piece);
     }
     if (comp.next_flag > 0 && !PlaceFlags(*ctx, plan->phases.back())) {
       return absl::InternalError("push variant: flag area overflow");

@@ -48,7 +48,7 @@ void BuildLaunches(Plan* plan) {
       a.timeout_ns = ctx->timeout_ns;
       a.ll_parity_stride = ctx->LLRegionBytes();
       a.flag_chunk = static_cast<uint32_t>(ctx->flag_chunk);
-      a.recv_piece = plan->recv_piece;
+      a.recv_piece = rsx.recv_piece;
       if (ctx->world > 1) {
         for (int q = 0; q < ctx->world; ++q) {
           if (q == r) continue;

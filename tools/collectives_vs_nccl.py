@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--push-min-bytes", type=int, default=None, help="context push threshold (-1 = never push)")
     ap.add_argument("--wave-bytes", type=int, default=None, help="push waves (0 = one wave)")
     ap.add_argument("--ll-max-bytes", type=int, default=None, help="one-shot budget (0 = never one-shot)")
+    ap.add_argument("--reduce-wave-bytes", type=int, default=None, help="Reduce push waves")
     args = ap.parse_args()
     if args.nvls:
         os.environ["RS_NVLS"] = "1"
@@ -45,6 +46,8 @@ def main():
         ctx.set_option("push_wave_bytes", args.wave_bytes)
     if args.ll_max_bytes is not None:
         ctx.set_option("ll_max_bytes", args.ll_max_bytes)
+    if args.reduce_wave_bytes is not None:
+        ctx.set_option("reduce_wave_bytes", args.reduce_wave_bytes)
     g = list(range(world))
     ops = args.ops.split(",")
     modes = [int(m) for m in args.reduce_modes.split(",")]
