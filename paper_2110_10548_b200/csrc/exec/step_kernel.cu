@@ -292,6 +292,8 @@ __device__ __forceinline__ void Store32(void* p, const Vec32& v) {
 // batches; they are read-heavy and already near the HBM rate).
 template <int kU>
 __device__ __forceinline__ void CopyChunk32(const Task& t, void* const* ptrs, uint64_t begin, uint64_t end) {
+  // task fields as locals: the stores' "memory" clobber would reload them per loop
+  const int nsrc = t.nsrc, ndst = t.ndst;
   uint64_t off[kU];
   bool ok[kU];
 #pragma unroll
@@ -300,7 +302,7 @@ __device__ __forceinline__ void CopyChunk32(const Task& t, void* const* ptrs, ui
     ok[u] = off[u] < end;
   }
   void* const* src = ptrs + t.ptr_begin;
-  void* const* dst = src + t.nsrc;
+  void* const* dst = src + nsrc;
   Vec32 raw[kU];
   const char* s0 = static_cast<const char*>(src[0]);
 #pragma unroll
@@ -308,7 +310,7 @@ __device__ __forceinline__ void CopyChunk32(const Task& t, void* const* ptrs, ui
     raw[u] = Vec32{make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};  // defined on every path (no spills)
     if (ok[u]) raw[u] = LoadStream32(s0 + off[u]);
   }
-  for (int j = 0; j < t.ndst; ++j) {
+  for (int j = 0; j < ndst; ++j) {
     char* d = static_cast<char*>(dst[j]);
 #pragma unroll
     for (int u = 0; u < kU; ++u)
@@ -398,6 +400,8 @@ __device__ __forceinline__ void WideChunk32(const Task& t, void* const* ptrs, ui
 // VectorChunk<DT, 2 kU> but 32 bytes per memory instruction.
 template <int DT, int kU>
 __device__ __forceinline__ void SumChunk32(const Task& t, void* const* ptrs, uint64_t begin, uint64_t end) {
+  // task fields as locals: the stores' "memory" clobber would reload them per loop
+  const int nsrc = t.nsrc, ndst = t.ndst;
   using Acc = typename AccOf<DT>::T;
   uint64_t off[kU];
   bool ok[kU];
@@ -407,7 +411,7 @@ __device__ __forceinline__ void SumChunk32(const Task& t, void* const* ptrs, uin
     ok[u] = off[u] < end;
   }
   void* const* src = ptrs + t.ptr_begin;
-  void* const* dst = src + t.nsrc;
+  void* const* dst = src + nsrc;
   Vec32 raw[kU];
   const char* s0 = static_cast<const char*>(src[0]);
 #pragma unroll
@@ -421,7 +425,7 @@ __device__ __forceinline__ void SumChunk32(const Task& t, void* const* ptrs, uin
     acc[2 * u].Init(raw[u].lo);
     acc[2 * u + 1].Init(raw[u].hi);
   }
-  for (int i = 1; i < t.nsrc; ++i) {
+  for (int i = 1; i < nsrc; ++i) {
     const char* si = static_cast<const char*>(src[i]);
 #pragma unroll
     for (int u = 0; u < kU; ++u)
@@ -434,7 +438,7 @@ __device__ __forceinline__ void SumChunk32(const Task& t, void* const* ptrs, uin
   }
 #pragma unroll
   for (int u = 0; u < kU; ++u) raw[u] = Vec32{acc[2 * u].Pack(), acc[2 * u + 1].Pack()};
-  for (int j = 0; j < t.ndst; ++j) {
+  for (int j = 0; j < ndst; ++j) {
     char* d = static_cast<char*>(dst[j]);
 #pragma unroll
     for (int u = 0; u < kU; ++u)
