@@ -563,7 +563,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         host_in = {d: ctx.buffer(d, ELEMS, "bf16").cpu().pin_memory() for d in ctx.hosted_slots}
-        e2e_steps = max(2, min(args.steps, 4))
+        e2e_steps = max(2, min(args.steps, 8))  # the first upload and last download are not overlapped
         sets = [(ctx, plans)]
         if not args.e2e_serial:
             ctx_b = make_ctx()
