@@ -275,8 +275,8 @@ int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value) {
   } else if (k == "push_wave_bytes") {
     ctx->impl->push_wave_bytes = value <= 0 ? 0 : (static_cast<uint64_t>(value) & ~15ull);
   } else if (k == "reduce_mode") {
-    if (value < rs::kReduceAuto || value > rs::kReduceNvlsRoot) {
-      return Bad("reduce_mode must be -1 (auto), 0 (pull), 1 (push), 2 (nvls) or 3 (nvls root)");
+    if (value < rs::kReduceAuto || value > rs::kReducePushRootPulled) {
+      return Bad("reduce_mode must be -1 (auto), 0 (pull), 1 (push), 2 (nvls), 3 (nvls root) or 4 (push, root pulled)");
     }
     ctx->impl->reduce_mode = static_cast<int>(value);
   } else if (k == "reduce_push_min_bytes") {

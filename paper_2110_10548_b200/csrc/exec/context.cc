@@ -158,7 +158,7 @@ void ReadTimeoutEnv(Context* ctx) {
   }
   if (const char* env = std::getenv("RS_REDUCE_MODE")) {
     const int m = std::atoi(env);
-    if (m >= kReduceAuto && m <= kReduceNvlsRoot) ctx->reduce_mode = m;
+    if (m >= kReduceAuto && m <= kReducePushRootPulled) ctx->reduce_mode = m;
   }
 }
 

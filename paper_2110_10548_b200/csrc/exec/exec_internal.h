@@ -68,7 +68,8 @@ typedef int (*ExchangeFn)(const void* send, size_t bytes, void* recv, void* user
 
 // A pointer-table entry: slot `slot`'s buffer (region -1) or its scratch
 // region `region`.
-enum { kReduceAuto = -1, kReducePull = 0, kReducePush = 1, kReduceNvls = 2, kReduceNvlsRoot = 3 };
+enum { kReduceAuto = -1, kReducePull = 0, kReducePush = 1, kReduceNvls = 2, kReduceNvlsRoot = 3,
+       kReducePushRootPulled = 4 };
 constexpr int kMcRegion = -2;  // Ref{mc group index, kMcRegion}: a multicast base
 // Ref{source slot, kLLRegion, receiver, sender, off}: packets of the source
 // slot's data in the receiver rank's LL area, sender's block, parity-0

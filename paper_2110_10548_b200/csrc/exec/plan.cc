@@ -217,7 +217,7 @@ struct Compiler {
   template <typename DstOf>
   void Sums(StepTasks& out, const std::vector<int>& g, const std::vector<int>& owner_idx,
             const std::vector<std::vector<Range>>& parts, bool push, DstOf dst_of,
-            uint64_t wave_bytes = ~0ull) {
+            uint64_t wave_bytes = ~0ull, const std::vector<uint8_t>& pulled = {}) {
     const int n = static_cast<int>(g.size());
     for (size_t j = 0; j < owner_idx.size(); ++j) {
       const int p = owner_idx[j];
@@ -241,7 +241,10 @@ struct Compiler {
           ProtoTask b{g[p], r, {}, dst_of(j)};
           b.wave = wave;
           for (int i = 0; i < n; ++i) {
-            if (i == p || ctx->slot_rank[g[i]] == rp) {
+            // read in place: the owner's own copy, co-located members, and
+            // members marked `pulled` (their copy is loaded remotely by the
+            // owner; ready since the step's entry barrier)
+            if (i == p || ctx->slot_rank[g[i]] == rp || (i < static_cast<int>(pulled.size()) && pulled[i])) {
               b.src.push_back(Buf(g[i]));
               b.src_flag.push_back(-1);
               continue;
@@ -493,9 +496,14 @@ struct Compiler {
         } else {
           for (int i = 1; i < n; ++i) owners.push_back(i);
         }
+        // kReducePushRootPulled: the owners load the root's copy remotely
+        // (the root's SMs issue nothing; its link serves the loads) and
+        // every other member lands its copy as in kReducePush.
+        std::vector<uint8_t> pulled(n, 0);
+        if (mode == kReducePushRootPulled) pulled[0] = 1;
         Sums(out, g, owners, SplitEven(ranges, static_cast<int>(owners.size())),
-             mode == kReducePush && PushSums(g, TotalBytes(ranges), 0), [&](size_t) { return root; },
-             ctx->reduce_wave_bytes);
+             (mode == kReducePush || mode == kReducePushRootPulled) && PushSums(g, TotalBytes(ranges), 0),
+             [&](size_t) { return root; }, ctx->reduce_wave_bytes, pulled);
         for (int r : rows) Vid(g[0], r) = next_id++;
         break;
       }

@@ -436,7 +436,7 @@ def test_copies_push_only_when_balanced():
     assert modes(d2, 1) <= {0}
 
 
-@pytest.mark.parametrize("mode", [1, 2, 3])
+@pytest.mark.parametrize("mode", [1, 2, 3, 4])
 @pytest.mark.parametrize("mapping", ["one_per_gpu", "four_gpus"])
 def test_reduce_modes_bit_exact_and_shaped(mode, mapping):
     """Reduce over >= 3 GPUs (semantics.cc:292-299): push (mode 1, store-only
@@ -467,7 +467,7 @@ def test_reduce_modes_bit_exact_and_shaped(mode, mapping):
                             seen += 1
                             assert mode >= 2 and dtype != numeric.I32
                             assert len(t["src"]) >= 4 and len(t["dst"]) == 1 and t["dst"][0] == t["src"][0]
-                        if mode == 1 and t.get("mode") in (3, 4):
+                        if mode in (1, 4) and t.get("mode") in (3, 4):
                             seen += 1
             inputs = numeric.synthetic_inputs(K, 4099, dtype)
             want = [x.copy() for x in inputs]
@@ -475,7 +475,7 @@ def test_reduce_modes_bit_exact_and_shaped(mode, mapping):
             got = [x.copy() for x in inputs]
             simulate_plan(desc, got, dtype)
             assert all(np.array_equal(a.view(np.uint8), b.view(np.uint8)) for a, b in zip(got, want)), prog.text
-    if mapping == "one_per_gpu" or mode == 1:
+    if mapping == "one_per_gpu" or mode in (1, 4):
         assert seen > 0
 
 
