@@ -76,3 +76,42 @@ def test_option_and_model_errors_on_a_planning_context():
     assert b"virtual" in lib.rs_last_error()
     plan.close()
     ctx.close()
+
+
+def test_emulated_context_argument_checks():
+    """rs_ctx_create_emulated validates its arguments before touching a GPU
+    (world in [2, RS_MAX_RANKS], slot ranks in range) and reports a status
+    without a GPU."""
+    lib = nat.lib()
+    h = ctypes.c_void_p()
+    assert lib.rs_ctx_create_emulated(4, None, 2, 0, 1 << 20, ctypes.byref(h)) == nat.RS_INVALID_ARGUMENT
+    assert lib.rs_ctx_create_emulated(4, nat.int_array([0, 0, 1, 1]), 1, 0, 1 << 20,
+                                      ctypes.byref(h)) == nat.RS_INVALID_ARGUMENT
+    assert b"world_size" in lib.rs_last_error()
+    assert lib.rs_ctx_create_emulated(4, nat.int_array([0, 0, 1, 1]), 9, 0, 1 << 20,
+                                      ctypes.byref(h)) == nat.RS_INVALID_ARGUMENT
+    import torch
+    if not torch.cuda.is_available():
+        code = lib.rs_ctx_create_emulated(4, nat.int_array([0, 0, 1, 1]), 2, 0, 1 << 20, ctypes.byref(h))
+        assert code in (nat.RS_UNAVAILABLE, nat.RS_INTERNAL, nat.RS_INVALID_ARGUMENT)
+
+
+def test_plan_options_validated():
+    """Named plan knobs (unroll, threads, max_ctas, wide_loads, dynamic_pieces,
+    pdl, local_wide, vec256, remote256) are accepted; unknown keys and bad
+    values are INVALID_ARGUMENT naming the valid keys."""
+    from paper_2110_10548_b200 import executor
+    from paper_2110_10548_b200.planner import LoweredProgram
+    ctx = executor.Context.virtual(4, [0, 1, 2, 3], 4)
+    plan = ctx.compile(LoweredProgram(steps=[(0, [[0, 1, 2, 3]])]), 1024, "f32")
+    lib = nat.lib()
+    for key, val in ((b"unroll", 8), (b"threads", 256), (b"max_ctas", 0), (b"wide_loads", 0), (b"dynamic_pieces", 1),
+                     (b"pdl", 0), (b"local_wide", 0), (b"vec256", 2), (b"remote256", 1)):
+        assert lib.rs_plan_set_option(plan._h, key, val) == nat.RS_OK, key
+    assert lib.rs_plan_set_option(plan._h, b"unroll", 3) == nat.RS_INVALID_ARGUMENT
+    assert lib.rs_plan_set_option(plan._h, b"bogus", 1) == nat.RS_INVALID_ARGUMENT
+    assert b"remote256" in lib.rs_last_error()
+    for key in (b"ll_total_bytes", b"reduce_push_min_bytes", b"reduce_wave_bytes", b"push_wave_bytes"):
+        assert lib.rs_ctx_set_option(ctx._h, key, 1 << 20) == nat.RS_OK, key
+    plan.close()
+    ctx.close()
