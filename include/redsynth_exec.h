@@ -128,7 +128,8 @@ int rs_ctx_local_ranks(rs_ctx* ctx, int* count, int* ordinals /* RS_MAX_RANKS */
  * (default: pull below "reduce_push_min_bytes" = 128 MiB, push with
  * "reduce_wave_bytes" = 4 MiB waves above), 0 pull, 1 push, 2 NVLS (members
  * reduce slices through the switch, store to the root; tolerance), 3 NVLS
- * with the root reducing everything. */
+ * with the root reducing everything, 4 push with the root's copy pulled by
+ * the owners (measured slower; kept for A/B). */
 int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value);
 
 /* NVLS (NVLink SHARP): with RS_NVLS=1 at context creation the heaps are
@@ -203,7 +204,9 @@ int rs_plan_set_launch(rs_plan* plan, int max_ctas, int threads);
  * "wide_loads" (cross-GPU sums load every source before adding; default 1),
  * "dynamic_pieces" (push phases take pieces from an atomic queue; default 1),
  * "pdl" (programmatic dependent launch; default 0, measured neutral),
- * "local_wide" (one-GPU sums load every source first; default 0). */
+ * "local_wide" (one-GPU sums load every source first; default 0),
+ * "vec256" (one-GPU 256-bit vectors: 0 off, 1 copies, 2 copies and sums;
+ * default 2), "remote256" (cross-GPU 256-bit vectors; default 1). */
 int rs_plan_set_option(rs_plan* plan, const char* key, long long value);
 
 /* JSON dump of the compiled plan: per step, per rank, the entry-barrier
