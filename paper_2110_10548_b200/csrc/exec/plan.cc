@@ -1040,10 +1040,15 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
     // parallelism for remote loads), between 4 KiB and kPieceBytes.
     std::vector<uint64_t> rank_bytes(R, 0);
     for (const ProtoTask& t : list) rank_bytes[ctx->slot_rank[t.owner]] += t.range.hi - t.range.lo;
+    uint32_t max_piece = kPieceBytes;  // RS_MAX_PIECE (A/B; power of two, 16 KiB .. 1 MiB)
+    if (const char* v = std::getenv("RS_MAX_PIECE")) {
+      const uint32_t m = static_cast<uint32_t>(std::strtoul(v, nullptr, 10));
+      if (m >= (16u << 10) && m <= (1u << 20) && (m & (m - 1)) == 0) max_piece = m;
+    }
     for (int r = 0; r < R; ++r) {
       const uint64_t sms = ctx->ranks[r].sm_count > 0 ? ctx->ranks[r].sm_count : kDefaultSmCount;
       uint32_t pb = 4u << 10;
-      while (pb < kPieceBytes && rank_bytes[r] / pb > 2 * sms) pb <<= 1;
+      while (pb < max_piece && rank_bytes[r] / pb > 2 * sms) pb <<= 1;
       plan->phases.back()[r].piece_bytes = pb;
       // Push reductions: 64 KiB pieces keep every CTA busy when results fan
       // out to n members (AllReduce, AllGather); a Reduce's owners store one
