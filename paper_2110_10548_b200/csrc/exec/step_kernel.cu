@@ -1061,7 +1061,7 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base, co
           done = true;
         }
       }
-      if constexpr (kNc) {
+      if constexpr (kNc && kUnroll == 8) {  // (unroll 4 + 256-bit: spills, measured -20 %)
         // one GPU, single-source copy with a 32-byte aligned body: 256-bit
         // vectors (kUnroll / 2 per thread, the same bytes in flight)
         if (!done && a.vec256 && ((t.lo | t.hi) & 31) == 0) {
