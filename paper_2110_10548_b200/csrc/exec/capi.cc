@@ -279,12 +279,14 @@ int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value) {
       return Bad("reduce_mode must be -1 (auto), 0 (pull), 1 (push), 2 (nvls), 3 (nvls root) or 4 (push, root pulled)");
     }
     ctx->impl->reduce_mode = static_cast<int>(value);
+  } else if (k == "nvls_bcast") {
+    ctx->impl->nvls_bcast = value != 0;
   } else if (k == "reduce_push_min_bytes") {
     ctx->impl->reduce_push_min_bytes = value < 0 ? ~0ull : static_cast<uint64_t>(value);
   } else if (k == "reduce_wave_bytes") {
     ctx->impl->reduce_wave_bytes = value <= 0 ? 0 : (static_cast<uint64_t>(value) & ~15ull);
   } else {
-    return Bad("unknown option (push_min_bytes | barrier_timeout_ms | nvls | nvls_min_group | nvls_min_bytes | ll_max_bytes | ll_total_bytes | reduce_mode | reduce_push_min_bytes | reduce_wave_bytes | push_wave_bytes)");
+    return Bad("unknown option (push_min_bytes | barrier_timeout_ms | nvls | nvls_min_group | nvls_min_bytes | ll_max_bytes | ll_total_bytes | nvls_bcast | reduce_mode | reduce_push_min_bytes | reduce_wave_bytes | push_wave_bytes)");
   }
   return RS_OK;
 }

@@ -46,6 +46,10 @@ constexpr uint16_t kModeFlagRecv = 4;
 // NVLS Reduce: ptrs[ptr_begin] is a multicast base; multimem.ld_reduce of
 // the task's range is stored (unicast) to the ndst destinations that follow.
 constexpr uint16_t kModeNvlsReduce = 5;
+// NVLS Broadcast: ptrs[ptr_begin] is the root's (local) buffer, ptrs[ptr_begin
+// + 1] a multicast base; the root's bytes are stored once to the multicast
+// address and the switch writes them into every member (bit copy).
+constexpr uint16_t kModeNvlsBroadcast = 6;
 
 // Everything one rank's kernel for one step needs (passed by value).
 struct StepArgs {

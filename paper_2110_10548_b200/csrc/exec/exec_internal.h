@@ -151,6 +151,10 @@ class Context {
   //                2425 us at 64 MiB / 256 MiB / 1 GiB, push with 4 MiB
   //                waves 194 / 554 / 1942 us.
   int reduce_mode = kReduceAuto;
+  // NVLS Broadcast (option "nvls_bcast"): on NVLS contexts, Broadcast groups
+  // that pass the NVLS size policy use one multicast store stream from the
+  // root instead of the P2P relay.
+  bool nvls_bcast = true;
   uint64_t reduce_push_min_bytes = 128ull << 20;
   uint64_t reduce_wave_bytes = 4ull << 20;
   // One-shot (LL) steps: when every cross-GPU group of a step has its members

@@ -47,6 +47,7 @@ struct ProtoTask {
   std::vector<Ref> dst;
   int mc = -1;  // >= 0: NVLS through multicast group mc (vector body)
   bool mc_reduce = false;  // NVLS Reduce: ld_reduce, unicast store to dst (else AllReduce)
+  bool mc_bcast = false;   // NVLS Broadcast: root's src[0] stored once to the multicast address
   // Push variant (one launch, chunk flags): a landing task (flag_send >= 0)
   // copies its vector body into the owner's memory chunk by chunk and raises
   // flag block `flag_send` per chunk; a reducing task waits for src_flag[i]
@@ -330,9 +331,9 @@ struct Compiler {
 
   // NVLS applies to AllReduce groups of >= nvls_min_group slots, one per GPU,
   // for floating-point data.
-  bool NvlsEligible(const std::vector<int>& g, uint64_t bytes) const {
+  bool NvlsEligible(const std::vector<int>& g, uint64_t bytes, bool any_dtype = false) const {
     const uint64_t min_bytes = g.size() >= 8 ? ctx->nvls_min_bytes_n8 : ctx->nvls_min_bytes;
-    if (!ctx->nvls || dtype == RS_I32 || bytes == 0 || bytes < min_bytes) return false;
+    if (!ctx->nvls || (dtype == RS_I32 && !any_dtype) || bytes == 0 || bytes < min_bytes) return false;
     if (static_cast<int>(g.size()) < ctx->nvls_min_group) return false;
     if (ctx->mc_groups.size() >= kMaxMcGroups && !ctx->mc_groups.count(g)) return false;
     std::vector<int> ranks;
@@ -517,7 +518,33 @@ struct Compiler {
       }
       case Collective::kBroadcast: {
         std::vector<std::pair<int, int>> row_holder;
-        for (int r : HeldRows(pre, g[0])) row_holder.push_back({r, g[0]});
+        const std::vector<int> rows = HeldRows(pre, g[0]);
+        for (int r : rows) row_holder.push_back({r, g[0]});
+        // NVLS: the root stores each byte once to the multicast address and
+        // the switch writes every member (bit-exact; any dtype). Only when
+        // every member needs every row (no content-id skips).
+        bool all_new = true;
+        for (int r : rows)
+          for (size_t i = 1; i < g.size(); ++i) all_new = all_new && Vid(g[i], r) != Vid(g[0], r);
+        const std::vector<Range> ranges = geo.Ranges(rows);
+        int mc = -1;
+        if (all_new && ctx->nvls_bcast && NvlsEligible(g, TotalBytes(ranges), /*any_dtype=*/true) &&
+            !EnsureMulticast(ctx, g, &mc).ok()) {
+          ctx->nvls = false;  // consistent P2P fallback on every rank
+          mc = -1;
+        }
+        if (mc >= 0) {
+          std::vector<Ref> others;
+          for (size_t i = 1; i < g.size(); ++i) others.push_back(Buf(g[i]));
+          for (const Range& r : ranges) {
+            ProtoTask t{g[0], r, {Buf(g[0])}, others, mc};
+            t.mc_bcast = true;
+            out.b.push_back(std::move(t));
+          }
+          for (int r : rows)
+            for (size_t i = 1; i < g.size(); ++i) Vid(g[i], r) = Vid(g[0], r);
+          break;
+        }
         Copies(out, g, row_holder);
         break;
       }
@@ -529,6 +556,18 @@ struct Compiler {
 void AddTraffic(std::vector<RankStep>& per_rank, const Context& ctx, const ProtoTask& t) {
   const double b = static_cast<double>(t.range.hi - t.range.lo);
   const int o = ctx.slot_rank[t.owner];
+  if (t.mc >= 0 && t.mc_bcast) {
+    // The root reads its copy and sends it once (tx b); the switch writes
+    // every member (rx b each, HBM b each).
+    per_rank[o].tx_bytes += b;
+    per_rank[o].hbm_bytes += 2 * b;
+    for (const Ref& y : t.dst) {
+      const int ry = ctx.slot_rank[y.slot];
+      per_rank[ry].rx_bytes += b;
+      per_rank[ry].hbm_bytes += b;
+    }
+    return;
+  }
   if (t.mc >= 0 && t.mc_reduce) {
     // Switch reads every member's copy (tx b each) and returns the sum to the
     // owner (rx b); the owner stores it to the root (unicast).
@@ -695,6 +734,17 @@ void Lay(RankStep& rs, const ProtoTask& t, uint32_t piece_bytes, uint64_t flag_c
     task.piece_begin = rs.npieces;
     task.ptr_begin = static_cast<uint32_t>(rs.ptr_refs.size());
     task.vec = vec ? 1u : 0u;
+    if (vec && t.mc >= 0 && t.mc_bcast) {
+      // NVLS Broadcast body: the root's buffer, then the multicast base.
+      task.mode = kModeNvlsBroadcast;
+      task.nsrc = 2;
+      task.ndst = 0;
+      rs.ptr_refs.push_back(t.src[0]);
+      rs.ptr_refs.push_back(Ref{t.mc, kMcRegion});
+      rs.npieces += static_cast<uint32_t>((hi - lo + piece_bytes - 1) / piece_bytes);
+      rs.tasks.push_back(task);
+      return;
+    }
     if (vec && t.mc >= 0) {
       // NVLS body: one multicast base pointer (unaligned edges stay ordered
       // P2P sums); a Reduce body also lists its unicast destinations.

@@ -88,7 +88,7 @@ void BuildLaunches(Plan* plan) {
       a.num_steps = static_cast<uint32_t>(P);
       a.piece_counter = reinterpret_cast<unsigned int*>(rank.heap + kPieceCounterOffset);
       for (const Task& t : rsx.tasks) {
-        a.has_nvls |= (t.mode == kModeNvlsAllReduce || t.mode == kModeNvlsReduce) ? 1u : 0u;
+        a.has_nvls |= (t.mode == kModeNvlsAllReduce || t.mode == kModeNvlsReduce || t.mode == kModeNvlsBroadcast) ? 1u : 0u;
         a.has_ll |= t.mode == kModeLL ? 1u : 0u;
         a.dynamic |= (plan->dynamic_pieces && (t.mode == kModeFlagSend || t.mode == kModeFlagRecv)) ? 1u : 0u;
       }
@@ -222,6 +222,14 @@ std::string DescribePlan(const Plan& plan) {
           tasks.push_back({{"lo", t.lo}, {"hi", t.hi}, {"vec", t.vec}, {"mode", t.mode},
                            {"piece_begin", t.piece_begin}, {"src", src}, {"dst", dst}, {"src_region", src_region},
                            {"dst_region", dst_region}, {"sends", sends}});
+          continue;
+        }
+        if (t.mode == kModeNvlsBroadcast) {
+          const McGroup* mc = plan.ctx->mc_index[r.ptr_refs[t.ptr_begin + 1].slot];
+          std::vector<int> mdst(mc->slots.begin() + 1, mc->slots.end());
+          tasks.push_back({{"lo", t.lo}, {"hi", t.hi}, {"vec", t.vec}, {"mode", t.mode},
+                           {"piece_begin", t.piece_begin}, {"src", std::vector<int>{mc->slots[0]}}, {"dst", mdst},
+                           {"src_region", std::vector<int>{-1}}, {"dst_region", std::vector<int>(mdst.size(), -1)}});
           continue;
         }
         if (t.mode == kModeNvlsAllReduce || t.mode == kModeNvlsReduce) {

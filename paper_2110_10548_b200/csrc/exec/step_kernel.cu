@@ -573,6 +573,30 @@ __device__ __forceinline__ void NvlsReduceChunk(const Task& t, void* const* ptrs
   }
 }
 
+// NVLS Broadcast chunk: weak loads of the root's data, one store per vector
+// to the multicast address (the switch replicates it into every member).
+template <int kUnroll>
+__device__ __forceinline__ void NvlsBroadcastChunk(const Task& t, void* const* ptrs, uint64_t begin,
+                                                   uint64_t end) {
+  const char* src = static_cast<const char*>(ptrs[t.ptr_begin]);
+  char* mc = static_cast<char*>(ptrs[t.ptr_begin + 1]);
+  uint4 v[kUnroll];
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {
+    v[u] = make_uint4(0, 0, 0, 0);
+    const uint64_t off = begin + (static_cast<uint64_t>(u) * blockDim.x + threadIdx.x) * 16u;
+    if (off < end) v[u] = LoadStream<false>(src + off);
+  }
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {
+    const uint64_t off = begin + (static_cast<uint64_t>(u) * blockDim.x + threadIdx.x) * 16u;
+    if (off >= end) continue;
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc + off), "r"(v[u].x),
+                 "r"(v[u].y), "r"(v[u].z), "r"(v[u].w)
+                 : "memory");
+  }
+}
+
 __device__ __forceinline__ void FenceProxyAlias() { asm volatile("fence.proxy.alias;" ::: "memory"); }
 
 // A scalar task (< 16 bytes): one element per thread.
@@ -1037,6 +1061,12 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base, co
         } else if (t.mode == kModeNvlsReduce) {
           for (uint64_t c = begin; c < end; c += chunk)
             NvlsReduceChunk<DT, kUnroll>(t, a.ptrs, c, min(end, c + chunk));
+          done = true;
+        }
+      }
+      if constexpr (!kNc) {
+        if (t.mode == kModeNvlsBroadcast) {  // a bit copy: every dtype
+          for (uint64_t c = begin; c < end; c += chunk) NvlsBroadcastChunk<kUnroll>(t, a.ptrs, c, min(end, c + chunk));
           done = true;
         }
       }

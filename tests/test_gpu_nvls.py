@@ -203,3 +203,34 @@ def test_nvls_one_process_per_gpu(tmp_path):
     for r in range(world):
         text = (tmp_path / f"r{r}.txt").read_text()
         assert text == "OK", text
+
+
+def test_nvls_broadcast_bit_exact(nvls_ctx):
+    """NVLS Broadcast (the root's bytes stored once to the multicast address,
+    the switch writes every member) is a bit copy: programs whose only
+    multicast steps are Broadcasts stay bit-exact for every dtype, and the
+    Broadcast steps really use multicast tasks (mode 6)."""
+    from paper_2110_10548_b200.planner import LoweredProgram
+    ctx, n = nvls_ctx
+    g = list(range(n))
+    prog = LoweredProgram(steps=[(3, [g]), (4, [g])])  # Reduce then Broadcast
+    for dtype in (numeric.I32, numeric.BF16, numeric.F32):
+        for N in (4099, (8 << 20) + 5):
+            ctx.set_option("reduce_mode", 0)  # exact P2P Reduce; NVLS only in the Broadcast
+            inputs = numeric.synthetic_inputs(n, N, dtype)
+            for d in range(n):
+                ctx.write(d, inputs[d])
+            plan = ctx.compile(prog, N, dtype)
+            desc = plan.describe()
+            modes = {t["mode"] for rk in desc["steps"][1]["ranks"] for t in rk["tasks"]}
+            assert 6 in modes, modes
+            for _ in range(2):
+                plan.run()
+            ctx.synchronize()
+            want = [x.copy() for x in inputs]
+            for _ in range(2):
+                numeric.execute(prog, n, want, dtype)
+            for d in range(n):
+                assert np.array_equal(ctx.read(d, N * ES[dtype]), want[d].view(np.uint8)), (dtype, N, d)
+            plan.close()
+    ctx.set_option("reduce_mode", -1)

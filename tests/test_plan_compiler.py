@@ -542,3 +542,33 @@ def test_push_waves_bit_exact_and_ordered(mapping, reduce_mode):
         simulate_plan(desc, got, numeric.BF16)
         assert all(np.array_equal(a.view(np.uint8), b.view(np.uint8)) for a, b in zip(got, want)), prog.text
     assert waves > 0
+
+
+def test_nvls_broadcast_plan_virtual():
+    """With NVLS on, Broadcast groups on distinct GPUs whose members all need
+    every row become one multicast store stream from the root (mode 6, any
+    dtype); the ordered simulation equals the oracle bit for bit."""
+    K, progs = golden_programs("k4_sock")
+    ctx = executor.Context.virtual(K, list(range(K)), K)
+    ctx.set_option("nvls", 1)
+    ctx.set_option("nvls_min_bytes", 0)
+    ctx.set_option("ll_max_bytes", 0)
+    seen = 0
+    for _, _, prog, _ in progs:
+        if not any(op == 4 for op, _ in prog.steps):
+            continue
+        for dtype in (numeric.I32, numeric.BF16):
+            desc = ctx.compile(prog, 4099, dtype).describe()
+            for st, (op, groups) in zip(desc["steps"], prog.steps):
+                for rk in st["ranks"]:
+                    for t in rk["tasks"]:
+                        if t.get("mode") == 6:
+                            seen += 1
+                            assert op == 4 and len(t["src"]) == 1 and len(t["dst"]) == len(groups[0]) - 1
+            inputs = numeric.synthetic_inputs(K, 4099, dtype)
+            want = [x.copy() for x in inputs]
+            numeric.execute(prog, K, want, dtype, nthreads=1)
+            got = [x.copy() for x in inputs]
+            simulate_plan(desc, got, dtype)
+            assert all(np.array_equal(a.view(np.uint8), b.view(np.uint8)) for a, b in zip(got, want)), prog.text
+    assert seen > 0

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--wave-bytes", type=int, default=None, help="push waves (0 = one wave)")
     ap.add_argument("--ll-max-bytes", type=int, default=None, help="one-shot budget (0 = never one-shot)")
     ap.add_argument("--reduce-wave-bytes", type=int, default=None, help="Reduce push waves")
+    ap.add_argument("--bcast-nvls", type=int, default=0, help="with --nvls: Broadcast by multicast stores")
     args = ap.parse_args()
     if args.nvls:
         os.environ["RS_NVLS"] = "1"
@@ -52,7 +53,9 @@ def main():
     ops = args.ops.split(",")
     modes = [int(m) for m in args.reduce_modes.split(",")]
     progs = {"AllReduce": LoweredProgram(steps=[(0, [g])]), "ReduceScatter": LoweredProgram(steps=[(1, [g])]),
-             "Reduce": LoweredProgram(steps=[(3, [g])])}
+             "Reduce": LoweredProgram(steps=[(3, [g])]),
+             # Reduce then Broadcast (a Broadcast needs a step that empties members first)
+             "ReduceBroadcast": LoweredProgram(steps=[(3, [g]), (4, [g])])}
     progs = {k: v for k, v in progs.items() if k in ops}
 
     def timed(fn):
@@ -90,15 +93,18 @@ def main():
         out = torch.empty(elems // world, device=dev, dtype=torch.bfloat16)
         nccl = {"AllReduce": lambda: dist.all_reduce(x),
                 "ReduceScatter": lambda: dist.reduce_scatter_tensor(out, x),
-                "Reduce": lambda: dist.reduce(x, dst=0)}
+                "Reduce": lambda: dist.reduce(x, dst=0),
+                "ReduceBroadcast": lambda: (dist.reduce(x, dst=0), dist.broadcast(x, src=0))}
         row = {"bytes": size}
         for name, prog in progs.items():
             theirs = timed(nccl[name])
             for mode in (modes if name == "Reduce" else [None]):
                 if mode is not None:
                     ctx.set_option("reduce_mode", mode)
-                if args.nvls:  # NVLS only where a Reduce mode asks for it (AllReduce stays P2P below 8 GPUs)
-                    ctx.set_option("nvls_min_bytes", 0 if mode in (2, 3) else -1)
+                if args.nvls:  # NVLS only where a Reduce mode or --bcast-nvls asks for it
+                    bc = name == "ReduceBroadcast" and args.bcast_nvls
+                    ctx.set_option("nvls_min_bytes", 0 if (mode in (2, 3) or bc) else -1)
+                    ctx.set_option("nvls_bcast", 1 if bc else 0)
                 plan = ctx.compile(prog, elems, "bf16")
                 ours = timed(plan.run)
                 used = sorted({t["mode"] for st in plan.describe()["steps"] for rk in st["ranks"] for t in rk["tasks"]})
