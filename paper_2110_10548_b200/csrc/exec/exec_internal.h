@@ -154,7 +154,7 @@ class Context {
   // NVLS Broadcast (option "nvls_bcast"): on NVLS contexts, Broadcast groups
   // that pass the NVLS size policy use one multicast store stream from the
   // root instead of the P2P relay.
-  bool nvls_bcast = true;
+  bool nvls_bcast = false;  // measured slower at K=4 (profiles/r02_bcast_nvls_k4.txt): opt-in
   uint64_t reduce_push_min_bytes = 128ull << 20;
   uint64_t reduce_wave_bytes = 4ull << 20;
   // One-shot (LL) steps: when every cross-GPU group of a step has its members

@@ -217,6 +217,7 @@ def test_nvls_broadcast_bit_exact(nvls_ctx):
     for dtype in (numeric.I32, numeric.BF16, numeric.F32):
         for N in (4099, (8 << 20) + 5):
             ctx.set_option("reduce_mode", 0)  # exact P2P Reduce; NVLS only in the Broadcast
+            ctx.set_option("nvls_bcast", 1)
             inputs = numeric.synthetic_inputs(n, N, dtype)
             for d in range(n):
                 ctx.write(d, inputs[d])
@@ -234,3 +235,4 @@ def test_nvls_broadcast_bit_exact(nvls_ctx):
                 assert np.array_equal(ctx.read(d, N * ES[dtype]), want[d].view(np.uint8)), (dtype, N, d)
             plan.close()
     ctx.set_option("reduce_mode", -1)
+    ctx.set_option("nvls_bcast", 0)

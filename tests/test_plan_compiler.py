@@ -551,6 +551,7 @@ def test_nvls_broadcast_plan_virtual():
     K, progs = golden_programs("k4_sock")
     ctx = executor.Context.virtual(K, list(range(K)), K)
     ctx.set_option("nvls", 1)
+    ctx.set_option("nvls_bcast", 1)
     ctx.set_option("nvls_min_bytes", 0)
     ctx.set_option("ll_max_bytes", 0)
     seen = 0
