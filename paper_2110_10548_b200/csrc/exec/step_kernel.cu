@@ -841,9 +841,12 @@ __device__ __forceinline__ void LLReceive(const Task& t, void* const* ptrs, uint
     LLReceiveWide<DT>(t, src, dst, local, begin, end, flag, parity_off, timeout_ns, error_flag);
     return;
   }
+  // bf16 keeps only the f32 accumulators and the last source's packets (a
+  // single source is then stored raw); the other dtypes accumulate in `out`.
+  constexpr bool kF32Acc = DT == RS_BF16;
   for (uint64_t x0 = begin + static_cast<uint64_t>(threadIdx.x) * 8u; x0 < end; x0 += stride * kLLBatch) {
-    uint2 mine[kLLBatch], out[kLLBatch];
-    float f[kLLBatch][4];
+    uint2 mine[kLLBatch], out[kF32Acc ? 1 : kLLBatch], v[kLLBatch];
+    float f[kF32Acc ? kLLBatch : 1][4];
 #pragma unroll
     for (int b = 0; b < kLLBatch; ++b) {
       const uint64_t x = x0 + b * stride;
@@ -852,7 +855,6 @@ __device__ __forceinline__ void LLReceive(const Task& t, void* const* ptrs, uint
     // Sum in source order; a single source is a raw copy.
     for (int i = 0; i < t.nsrc; ++i) {
       const uintptr_t s = reinterpret_cast<uintptr_t>(src[i]);
-      uint2 v[kLLBatch];
       if (s & 1u) {
         const char* base = reinterpret_cast<const char*>((s & ~uintptr_t{1}) + parity_off);
         uint4 pk[kLLBatch];
@@ -875,20 +877,24 @@ __device__ __forceinline__ void LLReceive(const Task& t, void* const* ptrs, uint
       }
 #pragma unroll
       for (int b = 0; b < kLLBatch; ++b) {
-        if constexpr (DT == RS_BF16) {
+        if constexpr (kF32Acc) {
           float g[4];
           BF16Acc::Widen(v[b].x, g[0], g[1]);
           BF16Acc::Widen(v[b].y, g[2], g[3]);
 #pragma unroll
           for (int k = 0; k < 4; ++k) f[b][k] = i == 0 ? g[k] : __fadd_rn(f[b][k], g[k]);
+        } else {
+          out[b] = i == 0 ? v[b] : AddPacket<DT>(out[b], v[b]);
         }
-        out[b] = i == 0 ? v[b] : AddPacket<DT>(out[b], v[b]);
       }
     }
 #pragma unroll
     for (int b = 0; b < kLLBatch; ++b) {
-      if constexpr (DT == RS_BF16) {
-        if (t.nsrc > 1) out[b] = make_uint2(BF16Acc::Narrow(f[b][0], f[b][1]), BF16Acc::Narrow(f[b][2], f[b][3]));
+      uint2 o;
+      if constexpr (kF32Acc) {
+        o = t.nsrc > 1 ? make_uint2(BF16Acc::Narrow(f[b][0], f[b][1]), BF16Acc::Narrow(f[b][2], f[b][3])) : v[b];
+      } else {
+        o = out[b];
       }
       const uint64_t x = x0 + b * stride;
       if (x >= end) continue;
@@ -898,11 +904,11 @@ __device__ __forceinline__ void LLReceive(const Task& t, void* const* ptrs, uint
         if (d & 1u) continue;
         char* base = reinterpret_cast<char*>(d);
         if (whole) {
-          *reinterpret_cast<uint2*>(base + x) = out[b];
+          *reinterpret_cast<uint2*>(base + x) = o;
           continue;
         }
         // Edge packet: only the elements inside [lo, hi).
-        const char* bytes = reinterpret_cast<const char*>(&out[b]);
+        const char* bytes = reinterpret_cast<const char*>(&o);
         for (uint32_t e = 0; e < 8; e += kEs) {
           if (x + e < t.lo || x + e >= t.hi) continue;
           if (kEs == 2) *reinterpret_cast<uint16_t*>(base + x + e) = *reinterpret_cast<const uint16_t*>(bytes + e);
