@@ -152,3 +152,39 @@ def test_emulated_ranks_every_program(world):
         for c in ctxs.values():
             c.close()
     assert all(used.get(v, 0) > 0 for v in ("ll", "pull", "push")), used
+
+
+@pytest.mark.timeout(1200)
+def test_reference_multinode_config_k32_on_one_gpu():
+    """The reference's two-node A100 machine (a100_2node.json, axes [8,4],
+    reduce {0}: 32 program devices, 254 programs): every program in local mode
+    (32 slots on one GPU) and a sample with the 32 slots spread over 8
+    emulated ranks (pull and push), bit-exact for bf16 and int32."""
+    K, progs = golden_programs("a100_2node_r0")
+    assert K == 32
+    ctx = executor.Context.local(K, [0] * K, max_bytes=1 << 20)
+    try:
+        for dt, N in ((numeric.BF16, 2053), (numeric.I32, 1031)):
+            inputs = numeric.synthetic_inputs(K, N, dt)
+            for _, _, prog, _ in progs:
+                for d in range(K):
+                    ctx.write(d, inputs[d])
+                plan = ctx.compile(prog, N, dt)
+                plan.run()
+                ctx.synchronize()
+                want = [x.copy() for x in inputs]
+                numeric.execute(prog, K, want, dt)
+                for d in range(K):
+                    assert np.array_equal(ctx.read(d, N * ES[dt]), want[d].view(np.uint8)), (prog.text, d)
+                plan.close()
+    finally:
+        ctx.close()
+    ctxs, used = {}, {}
+    try:
+        for variant, N, dt in (("pull", 3001, numeric.BF16), ("push", (1 << 16) + 3, numeric.I32)):
+            _run_case(ctxs, 8, {"set": "a100_2node_r0", "K": 32, "N": N, "dtype": dt, "variant": variant,
+                                "stride": 9, "runs": 1}, used)
+    finally:
+        for c in ctxs.values():
+            c.close()
+    assert used.get("pull", 0) > 0 and used.get("push", 0) > 0, used

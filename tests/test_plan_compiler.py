@@ -573,3 +573,24 @@ def test_nvls_broadcast_plan_virtual():
             simulate_plan(desc, got, dtype)
             assert all(np.array_equal(a.view(np.uint8), b.view(np.uint8)) for a, b in zip(got, want)), prog.text
     assert seen > 0
+
+
+@pytest.mark.parametrize("world", [1, 4, 8])
+def test_reference_multinode_config_k32(world):
+    """The reference's own two-node A100 machine (configs/a100_2node.json,
+    axes [8,4], reduce {0}: K = 32 program devices, 254 programs) compiled
+    for 32 slots on 1, 4 or 8 ranks: hazard-free plans equal to the oracle."""
+    K, progs = golden_programs("a100_2node_r0")
+    assert K == 32
+    slot_rank = [d * world // K for d in range(K)]
+    ctx = executor.Context.virtual(K, slot_rank, world)
+    if world > 1:
+        ctx.set_option("push_min_bytes", 0)
+    for _, _, prog, _ in progs[::(1 if world == 1 else 5)]:
+        desc = ctx.compile(prog, 1031, numeric.BF16).describe()
+        inputs = numeric.synthetic_inputs(K, 1031, numeric.BF16)
+        want = [x.copy() for x in inputs]
+        numeric.execute(prog, K, want, numeric.BF16, nthreads=1)
+        got = [x.copy() for x in inputs]
+        simulate_plan(desc, got, numeric.BF16)
+        assert all(np.array_equal(a.view(np.uint8), b.view(np.uint8)) for a, b in zip(got, want)), prog.text
