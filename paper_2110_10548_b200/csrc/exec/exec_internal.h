@@ -231,6 +231,7 @@ class Plan {
   int ctas_per_sm = 0;  // resident capacity for (dtype, threads, unroll); 0 = recompute
   uint32_t recv_piece = kFlagChunk;  // effective push reducing piece of this plan
   bool dynamic_pieces = true;
+  bool local_dynamic = false;  // one-GPU phases take pieces from a prefetched atomic queue (RS_LOCAL_DYNAMIC, A/B)
   bool pdl = false;  // programmatic dependent launch of every step (option "pdl", env RS_PDL): measured neutral
   // cross-GPU pull sums, push landing copies and push reductions with 256-bit
   // vectors (option "remote256", env RS_REMOTE256): K=4 pull 16-256 MiB

@@ -1133,7 +1133,23 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base, co
     __syncthreads();
     return q;
   };
-  for (uint32_t p = a.dynamic ? next(0) : cta; p < a.npieces; p = next(p)) run_piece(p);
+  // a.dynamic == 2 (one-GPU phases, A/B local_dynamic): thread 0 reserves
+  // the next piece before working on the current one, so the atomic's round
+  // trip hides under the piece.
+  uint32_t p = a.dynamic ? next(0) : cta;
+  while (p < a.npieces) {
+    uint32_t reserved = 0;
+    if (a.dynamic == 2 && threadIdx.x == 0) reserved = atomicAdd(a.piece_counter, 1u);
+    run_piece(p);
+    if (a.dynamic == 2) {
+      if (threadIdx.x == 0) next_piece = reserved;
+      __syncthreads();
+      p = next_piece;
+      __syncthreads();
+    } else {
+      p = next(p);
+    }
+  }
   if (a.dynamic && threadIdx.x == 0 && atomicAdd(a.piece_counter + 1, 1u) == ncta - 1) {
     // last CTA out: reset the queue for the next launch on this rank
     atomicExch(a.piece_counter, 0u);
