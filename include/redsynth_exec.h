@@ -206,7 +206,9 @@ int rs_plan_set_launch(rs_plan* plan, int max_ctas, int threads);
  * "pdl" (programmatic dependent launch; default 0, measured neutral),
  * "local_wide" (one-GPU sums load every source first; default 0),
  * "vec256" (one-GPU 256-bit vectors: 0 off, 1 copies, 2 copies and sums;
- * default 2), "remote256" (cross-GPU 256-bit vectors; default 1). */
+ * default 2), "remote256" (cross-GPU 256-bit vectors; default 1),
+ * "piece_queue" (phases without chunk flags take pieces from a prefetched
+ * atomic queue: 0 never, 1 one-GPU contexts, 2 every context; default 1). */
 int rs_plan_set_option(rs_plan* plan, const char* key, long long value);
 
 /* JSON dump of the compiled plan: per step, per rank, the entry-barrier

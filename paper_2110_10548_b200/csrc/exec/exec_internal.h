@@ -231,14 +231,19 @@ class Plan {
   int ctas_per_sm = 0;  // resident capacity for (dtype, threads, unroll); 0 = recompute
   uint32_t recv_piece = kFlagChunk;  // effective push reducing piece of this plan
   bool dynamic_pieces = true;
-  bool local_dynamic = false;  // one-GPU phases take pieces from a prefetched atomic queue (RS_LOCAL_DYNAMIC, A/B)
+  // Phases without chunk flags take their pieces from a prefetched atomic
+  // queue instead of a static grid stride (option "piece_queue", env
+  // RS_PIECE_QUEUE): 0 never, 1 one-GPU contexts (default: N=1 config 2
+  // 2864 -> 3110 GB/s, same DRAM bytes, profiles/r02_piece_queue.txt),
+  // 2 also the pull / NVLS phases of multi-GPU contexts (A/B).
+  int piece_queue = 1;
   bool pdl = false;  // programmatic dependent launch of every step (option "pdl", env RS_PDL): measured neutral
   // cross-GPU pull sums, push landing copies and push reductions with 256-bit
   // vectors (option "remote256", env RS_REMOTE256): K=4 pull 16-256 MiB
   // AllReduce -2.5 %, ReduceScatter -4 %, Reduce -3 % (profiles/r02_remote256_ab.txt)
   bool remote256 = true;
   int vec256 = 2;  // one-GPU 256-bit vectors: 1 copies, 2 copies and sums (option "vec256", env RS_VEC256)
-  bool local_wide = false;  // one-GPU sums: all sources in flight (option "local_wide", env RS_LOCAL_WIDE)  // push phases take pieces from an atomic queue (option / env RS_DYNAMIC_PIECES)
+  bool local_wide = false;  // one-GPU sums: all sources in flight (option "local_wide", env RS_LOCAL_WIDE)
   bool wide_loads = true;  // cross-GPU pull sums: all sources in flight (option "wide_loads", env RS_WIDE_LOADS)
   // Launch phases, one per program step (every variant — pull, push with
   // chunk flags, one-shot, NVLS — runs its step in a single launch).

@@ -92,7 +92,8 @@ void BuildLaunches(Plan* plan) {
         a.has_ll |= t.mode == kModeLL ? 1u : 0u;
         a.dynamic |= (plan->dynamic_pieces && (t.mode == kModeFlagSend || t.mode == kModeFlagRecv)) ? 1u : 0u;
       }
-      if (plan->local_dynamic && ctx->world == 1) a.dynamic = 2;
+      if (a.dynamic == 0 && !a.has_ll && (plan->piece_queue >= 2 || (plan->piece_queue == 1 && ctx->world == 1)))
+        a.dynamic = 2;
       int resident = plan->ctas_per_sm * rank.sm_count;
       if (ctx->emulated) {
         // all ranks share one cooperative launch: split its co-resident CTAs

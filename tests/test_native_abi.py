@@ -98,7 +98,7 @@ def test_emulated_context_argument_checks():
 
 def test_plan_options_validated():
     """Named plan knobs (unroll, threads, max_ctas, wide_loads, dynamic_pieces,
-    pdl, local_wide, vec256, remote256) are accepted; unknown keys and bad
+    pdl, local_wide, vec256, remote256, piece_queue) are accepted; unknown keys and bad
     values are INVALID_ARGUMENT naming the valid keys."""
     from paper_2110_10548_b200 import executor
     from paper_2110_10548_b200.planner import LoweredProgram
@@ -106,11 +106,13 @@ def test_plan_options_validated():
     plan = ctx.compile(LoweredProgram(steps=[(0, [[0, 1, 2, 3]])]), 1024, "f32")
     lib = nat.lib()
     for key, val in ((b"unroll", 8), (b"threads", 256), (b"max_ctas", 0), (b"wide_loads", 0), (b"dynamic_pieces", 1),
-                     (b"pdl", 0), (b"local_wide", 0), (b"vec256", 2), (b"remote256", 1)):
+                     (b"pdl", 0), (b"local_wide", 0), (b"vec256", 2), (b"remote256", 1),
+                     (b"piece_queue", 2)):
         assert lib.rs_plan_set_option(plan._h, key, val) == nat.RS_OK, key
     assert lib.rs_plan_set_option(plan._h, b"unroll", 3) == nat.RS_INVALID_ARGUMENT
+    assert lib.rs_plan_set_option(plan._h, b"piece_queue", 3) == nat.RS_INVALID_ARGUMENT
     assert lib.rs_plan_set_option(plan._h, b"bogus", 1) == nat.RS_INVALID_ARGUMENT
-    assert b"remote256" in lib.rs_last_error()
+    assert b"piece_queue" in lib.rs_last_error()
     for key in (b"ll_total_bytes", b"reduce_push_min_bytes", b"reduce_wave_bytes", b"push_wave_bytes"):
         assert lib.rs_ctx_set_option(ctx._h, key, 1 << 20) == nat.RS_OK, key
     plan.close()
