@@ -233,9 +233,9 @@ class Plan {
   bool dynamic_pieces = true;
   // Phases without chunk flags take their pieces from a prefetched atomic
   // queue instead of a static grid stride (option "piece_queue", env
-  // RS_PIECE_QUEUE): 0 never, 1 one-GPU contexts (default: N=1 config 2
-  // 2864 -> 3110 GB/s, same DRAM bytes, profiles/r02_piece_queue.txt),
-  // 2 also the pull / NVLS phases of multi-GPU contexts (A/B).
+  // RS_PIECE_QUEUE): 0 never, 1 phases in which the rank touches only its
+  // own HBM (default: N=1 config 2 2864 -> 3110 GB/s, same DRAM bytes,
+  // profiles/r02_piece_queue.txt), 2 also pull and NVLS phases (A/B).
   int piece_queue = 1;
   bool pdl = false;  // programmatic dependent launch of every step (option "pdl", env RS_PDL): measured neutral
   // cross-GPU pull sums, push landing copies and push reductions with 256-bit

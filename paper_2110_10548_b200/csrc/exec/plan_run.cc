@@ -92,7 +92,11 @@ void BuildLaunches(Plan* plan) {
         a.has_ll |= t.mode == kModeLL ? 1u : 0u;
         a.dynamic |= (plan->dynamic_pieces && (t.mode == kModeFlagSend || t.mode == kModeFlagRecv)) ? 1u : 0u;
       }
-      if (a.dynamic == 0 && !a.has_ll && (plan->piece_queue >= 2 || (plan->piece_queue == 1 && ctx->world == 1)))
+      // piece_queue 1: this rank's phase touches only its own HBM (every
+      // phase of a one-GPU context, the GPU-local steps of multi-GPU ones);
+      // 2: also pull and NVLS phases.
+      const bool own_hbm = rsx.remote_peers == 0 && !a.has_nvls;
+      if (a.dynamic == 0 && !a.has_ll && (plan->piece_queue >= 2 || (plan->piece_queue == 1 && own_hbm)))
         a.dynamic = 2;
       int resident = plan->ctas_per_sm * rank.sm_count;
       if (ctx->emulated) {
