@@ -234,9 +234,11 @@ class Plan {
   // Phases without chunk flags take their pieces from a prefetched atomic
   // queue instead of a static grid stride (option "piece_queue", env
   // RS_PIECE_QUEUE): 0 never, 1 phases in which the rank touches only its
-  // own HBM (default: N=1 config 2 2864 -> 3110 GB/s, same DRAM bytes,
-  // profiles/r02_piece_queue.txt), 2 also pull and NVLS phases (A/B).
-  int piece_queue = 1;
+  // own HBM (N=1 config 2 2864 -> 3110 GB/s, same DRAM bytes), 2 (default)
+  // also pull and NVLS phases (N=2 1832 -> 1846, N=4 2131 -> 2150 GB/s, K=4
+  // Reduce 16-256 MiB -2..-12 % time); only phases with >= 2 pieces per CTA
+  // (profiles/r02_piece_queue.txt).
+  int piece_queue = 2;
   bool pdl = false;  // programmatic dependent launch of every step (option "pdl", env RS_PDL): measured neutral
   // cross-GPU pull sums, push landing copies and push reductions with 256-bit
   // vectors (option "remote256", env RS_REMOTE256): K=4 pull 16-256 MiB
