@@ -235,9 +235,9 @@ class Plan {
   // queue instead of a static grid stride (option "piece_queue", env
   // RS_PIECE_QUEUE): 0 never, 1 phases in which the rank touches only its
   // own HBM (N=1 config 2 2864 -> 3110 GB/s, same DRAM bytes), 2 (default)
-  // also pull and NVLS phases (N=2 1832 -> 1846, N=4 2131 -> 2150 GB/s, K=4
-  // Reduce 16-256 MiB -2..-12 % time); only phases with >= 2 pieces per CTA
-  // (profiles/r02_piece_queue.txt).
+  // also pull and NVLS phases (same-box ABAB: N=2 1818 -> 1843, N=4 2127 ->
+  // 2151 GB/s, K=4 collectives neutral); only phases with >= 2 pieces per
+  // CTA (profiles/r02_piece_queue.txt).
   int piece_queue = 2;
   bool pdl = false;  // programmatic dependent launch of every step (option "pdl", env RS_PDL): measured neutral
   // cross-GPU pull sums, push landing copies and push reductions with 256-bit
