@@ -213,9 +213,12 @@ std::string DescribePlan(const Plan& plan) {
   doc["slot_rank"] = plan.ctx->slot_rank;
   doc["scratch_regions"] = plan.ctx->scratch_regions;
   nlohmann::ordered_json phases = nlohmann::ordered_json::array();
-  for (const std::vector<RankStep>& per_rank : plan.phases) {
+  const size_t R = static_cast<size_t>(plan.ctx->world);
+  for (size_t ph = 0; ph < plan.phases.size(); ++ph) {
+    const std::vector<RankStep>& per_rank = plan.phases[ph];
     nlohmann::ordered_json ranks = nlohmann::ordered_json::array();
-    for (const RankStep& r : per_rank) {
+    for (size_t ri = 0; ri < per_rank.size(); ++ri) {
+      const RankStep& r = per_rank[ri];
       nlohmann::ordered_json tasks = nlohmann::ordered_json::array();
       for (const Task& t : r.tasks) {
         std::vector<int> src, dst, src_region, dst_region, sends;
@@ -262,6 +265,13 @@ std::string DescribePlan(const Plan& plan) {
       std::vector<int> wait(r.wait.begin(), r.wait.end());
       ranks.push_back({{"wait", wait}, {"signal", r.signal_done}, {"npieces", r.npieces}, {"tx", r.tx_bytes}, {"rx", r.rx_bytes},
                        {"hbm", r.hbm_bytes}, {"tasks", tasks}});
+      // After the first run on a driven rank: the launch shape and the piece
+      // schedule (0 static grid stride, 1 push queue, 2 prefetched queue).
+      const size_t k = ph * R + ri;
+      if (k < plan.launch_args.size() && plan.launch_args[k].piece_counter != nullptr) {
+        ranks.back()["grid"] = plan.launch_grid[k];
+        ranks.back()["queue"] = plan.launch_args[k].dynamic;
+      }
     }
     phases.push_back({{"ranks", ranks}});
   }

@@ -379,5 +379,7 @@ class Plan:
         nat.check(nat.lib().rs_plan_set_launch(self._h, int(max_ctas), int(threads)))
 
     def set_option(self, key: str, value: int):
-        """Named launch knobs: unroll (4|8), threads, max_ctas."""
+        """Named plan knobs (include/redsynth_exec.h rs_plan_set_option):
+        unroll (4|8), threads, max_ctas, wide_loads, dynamic_pieces, pdl,
+        local_wide, vec256, remote256, piece_queue (0|1|2)."""
         nat.check(nat.lib().rs_plan_set_option(self._h, key.encode(), int(value)))

@@ -83,6 +83,35 @@ def test_config2_full_size_bf16_local(local8):
         _run(local8, prog, K, N, numeric.BF16, inputs=inputs)
 
 
+@pytest.mark.parametrize("queue", [0, 1, 2])
+def test_piece_schedules_local(local8, queue):
+    """Static grid stride (piece_queue 0) and the prefetched atomic queue
+    (1, 2): the same bytes, bit-exact, replayed (the queue word resets at
+    the end of each launch). describe() after a run reports the schedule:
+    the queue only on phases with >= 2 pieces per CTA."""
+    K, progs = golden_programs("cfg2_r01")
+    for N in (12 << 20, 100003):
+        inputs = numeric.synthetic_inputs(K, N, numeric.BF16)
+        for _, _, prog, _ in progs[::125]:
+            for d in range(K):
+                local8.write(d, inputs[d])
+            plan = local8.compile(prog, N, numeric.BF16)
+            plan.set_option("piece_queue", queue)
+            for _ in range(3):
+                plan.run()
+            local8.synchronize()
+            want = [x.copy() for x in inputs]
+            for _ in range(3):
+                numeric.execute(prog, K, want, numeric.BF16)
+            for d in range(K):
+                assert np.array_equal(local8.read(d, N * 2), want[d].view(np.uint8)), (prog.text, queue, N, d)
+            for st in plan.describe()["steps"]:
+                rk = st["ranks"][0]
+                expect = 2 if queue and rk["npieces"] >= 2 * rk["grid"] else 0
+                assert rk["queue"] == expect, (prog.text, queue, N, rk["npieces"], rk["grid"], rk["queue"])
+            plan.close()
+
+
 @pytest.mark.parametrize("name", ["cfg3_r0", "cfg3_r1", "cfg3_r2", "cfg3_r01", "cfg3_r02", "cfg3_r12"])
 def test_config3_every_program_f32_local(local8, name):
     K, progs = golden_programs(name)
