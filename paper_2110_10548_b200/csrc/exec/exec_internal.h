@@ -235,7 +235,7 @@ class Plan {
   // queue instead of a static grid stride (option "piece_queue", env
   // RS_PIECE_QUEUE): 0 never, 1 phases in which the rank touches only its
   // own HBM (N=1 config 2 2864 -> 3110 GB/s, same DRAM bytes), 2 (default)
-  // also pull and NVLS phases (same-box ABAB: N=2 1818 -> 1843, N=4 2127 ->
+  // also pull phases (same-box ABAB: N=2 1818 -> 1843, N=4 2127 ->
   // 2151 GB/s, K=4 collectives neutral); only phases with >= 2 pieces per
   // CTA (profiles/r02_piece_queue.txt).
   int piece_queue = 2;

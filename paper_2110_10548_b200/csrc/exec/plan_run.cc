@@ -94,9 +94,10 @@ void BuildLaunches(Plan* plan) {
       }
       // piece_queue 1: this rank's phase touches only its own HBM (every
       // phase of a one-GPU context, the GPU-local steps of multi-GPU ones);
-      // 2: also pull and NVLS phases.
-      const bool own_hbm = rsx.remote_peers == 0 && !a.has_nvls;
-      if (a.dynamic == 0 && !a.has_ll && (plan->piece_queue >= 2 || (plan->piece_queue == 1 && own_hbm)))
+      // 2: also pull phases. NVLS and one-shot phases keep the static stride
+      // (NVLS was not A/B'd with the queue).
+      const bool own_hbm = rsx.remote_peers == 0;
+      if (a.dynamic == 0 && !a.has_ll && !a.has_nvls && (plan->piece_queue >= 2 || (plan->piece_queue == 1 && own_hbm)))
         a.dynamic = 2;
       int resident = plan->ctas_per_sm * rank.sm_count;
       if (ctx->emulated) {
