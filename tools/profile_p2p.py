@@ -24,6 +24,9 @@ def main():
     ap.add_argument("--program", type=int, default=0)
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--push", type=int, default=0, help="1: push variant (store-only), 0: pull")
+    ap.add_argument("--op", default=None, help="one collective over all GPUs instead of a synthesized program: "
+                                               "AllReduce | ReduceScatter | Reduce")
+    ap.add_argument("--reduce-mode", type=int, default=None, help="context reduce_mode (-1 auto, 0 pull, 1 push)")
     args = ap.parse_args()
     if os.environ.get("RS_SOLO_PROFILE") != "1":
         raise SystemExit("set RS_SOLO_PROFILE=1 (the kernels would wait for peers ncu never runs)")
@@ -36,12 +39,18 @@ def main():
     from paper_2110_10548_b200 import executor, planner
     n = args.gpus
     desc = {2: "b200_flat2", 4: "b200_flat4", 8: "b200_flat8"}[n]
-    prog = planner.synthesize(planner.config_path(desc), [n], [0]).placements[0].programs[args.program]
+    if args.op:
+        g = list(range(n))
+        prog = planner.LoweredProgram(steps=[({"AllReduce": 0, "ReduceScatter": 1, "Reduce": 3}[args.op], [g])])
+    else:
+        prog = planner.synthesize(planner.config_path(desc), [n], [0]).placements[0].programs[args.program]
     es = 2 if args.dtype == "bf16" else 4
     elems = (args.mib << 20) // es
     ctx = executor.Context.local(n, list(range(n)), args.mib << 20)
     ctx.set_option("ll_max_bytes", 0)  # one-shot receives wait for peer packets: not profilable alone
     ctx.set_option("push_min_bytes", 0 if args.push else -1)
+    if args.reduce_mode is not None:
+        ctx.set_option("reduce_mode", args.reduce_mode)
     plan = ctx.compile(prog, elems, args.dtype)
     print("program:", prog.text, "| per-step link bytes per GPU per direction:",
           [plan.step_bytes(s)[0] for s in range(len(prog.steps))], flush=True)
