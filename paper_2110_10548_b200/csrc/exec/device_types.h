@@ -61,7 +61,7 @@ struct StepArgs {
   int32_t dtype;
   unsigned int* arrive_counter;  // this rank's CTA-arrival counter
   unsigned int* piece_counter;   // [0] next piece, [1] CTAs done (dynamic push phases)
-  uint32_t dynamic;              // pieces handed out by piece_counter (push phases)
+  uint32_t dynamic;              // 0 static grid stride; pieces from piece_counter: 1 one atomic per piece, 2 next piece reserved ahead
   int* error_flag;               // set to 1 on a barrier timeout
   const uint64_t* inbox;         // this rank's flags, inbox[q] = last epoch of rank q
   uint64_t* signal_ptrs[RS_MAX_RANKS];  // &inbox_of_rank_q[my_rank], every other rank q

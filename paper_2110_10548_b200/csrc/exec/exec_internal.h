@@ -239,6 +239,11 @@ class Plan {
   // 2151 GB/s, K=4 collectives neutral); only phases with >= 2 pieces per
   // CTA (profiles/r02_piece_queue.txt).
   int piece_queue = 2;
+  // Push phases reserve their next piece ahead too (option "push_prefetch",
+  // env RS_PUSH_PREFETCH; A/B). Deadlock-free: pieces are still handed out
+  // in order, so a CTA holding a reserved landing piece of wave w waits only
+  // on landings of an earlier wave, which no CTA holds hostage in turn.
+  bool push_prefetch = false;
   bool pdl = false;  // programmatic dependent launch of every step (option "pdl", env RS_PDL): measured neutral
   // cross-GPU pull sums, push landing copies and push reductions with 256-bit
   // vectors (option "remote256", env RS_REMOTE256): K=4 pull 16-256 MiB

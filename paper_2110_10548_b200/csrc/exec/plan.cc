@@ -1008,6 +1008,7 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
   if (const char* v = std::getenv("RS_DYNAMIC_PIECES")) plan->dynamic_pieces = std::atoi(v) != 0;
   if (const char* v = std::getenv("RS_PDL")) plan->pdl = std::atoi(v) != 0;
   if (const char* v = std::getenv("RS_PIECE_QUEUE")) plan->piece_queue = std::atoi(v);
+  if (const char* v = std::getenv("RS_PUSH_PREFETCH")) plan->push_prefetch = std::atoi(v) != 0;
   if (const char* v = std::getenv("RS_LOCAL_WIDE")) plan->local_wide = std::atoi(v) != 0;
   if (const char* v = std::getenv("RS_VEC256")) plan->vec256 = std::atoi(v);
   if (const char* v = std::getenv("RS_REMOTE256")) plan->remote256 = std::atoi(v) != 0;

@@ -113,11 +113,13 @@ void BuildLaunches(Plan* plan) {
       // are better (652 vs 637 at K=2, r01_tune_n2.log).
       if (plan->max_ctas == 0 && !a.has_nvls && !a.has_ll && rsx.remote_peers >= 2) cap = std::min(cap, rank.sm_count);
       if (cap <= 0) cap = std::max(1, rank.sm_count);
+      const bool push_queue = a.dynamic == 1;  // ordering required: never static
+      if (push_queue && plan->push_prefetch) a.dynamic = 2;
       const int grid = std::max(1, std::min<int>(cap, static_cast<int>(rsx.npieces)));
       plan->launch_grid[static_cast<size_t>(ph) * R + r] = grid;
       // Under two pieces per CTA there is nothing to balance and the queue's
       // first atomic is pure latency (K=4 1 MiB AllReduce 16.6 -> 19.3 us).
-      if (a.dynamic == 2 && rsx.npieces < 2u * static_cast<uint32_t>(grid)) a.dynamic = 0;
+      if (a.dynamic == 2 && !push_queue && rsx.npieces < 2u * static_cast<uint32_t>(grid)) a.dynamic = 0;
     }
   }
 }

@@ -107,7 +107,7 @@ def test_plan_options_validated():
     lib = nat.lib()
     for key, val in ((b"unroll", 8), (b"threads", 256), (b"max_ctas", 0), (b"wide_loads", 0), (b"dynamic_pieces", 1),
                      (b"pdl", 0), (b"local_wide", 0), (b"vec256", 2), (b"remote256", 1),
-                     (b"piece_queue", 2)):
+                     (b"piece_queue", 2), (b"push_prefetch", 0)):
         assert lib.rs_plan_set_option(plan._h, key, val) == nat.RS_OK, key
     assert lib.rs_plan_set_option(plan._h, b"unroll", 3) == nat.RS_INVALID_ARGUMENT
     assert lib.rs_plan_set_option(plan._h, b"piece_queue", 3) == nat.RS_INVALID_ARGUMENT
