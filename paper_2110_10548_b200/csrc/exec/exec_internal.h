@@ -240,9 +240,12 @@ class Plan {
   // CTA (profiles/r02_piece_queue.txt).
   int piece_queue = 2;
   // Push phases reserve their next piece ahead too (option "push_prefetch",
-  // env RS_PUSH_PREFETCH; A/B). Deadlock-free: pieces are still handed out
-  // in order, so a CTA holding a reserved landing piece of wave w waits only
-  // on landings of an earlier wave, which no CTA holds hostage in turn.
+  // env RS_PUSH_PREFETCH). Deadlock-free (pieces are still handed out in
+  // order, so a CTA holding a reserved landing piece of wave w waits only on
+  // landings of an earlier wave) but slower: a CTA blocked on chunk flags
+  // holds its reserved landing piece back from the peers waiting for it (K=4
+  // 64 MiB AllReduce 165 -> 187 us, N=4 2152 -> 2103 GB/s,
+  // profiles/r02_piece_queue.txt). Off.
   bool push_prefetch = false;
   bool pdl = false;  // programmatic dependent launch of every step (option "pdl", env RS_PDL): measured neutral
   // cross-GPU pull sums, push landing copies and push reductions with 256-bit
