@@ -129,7 +129,9 @@ int rs_ctx_local_ranks(rs_ctx* ctx, int* count, int* ordinals /* RS_MAX_RANKS */
  * "reduce_wave_bytes" = 4 MiB waves above), 0 pull, 1 push, 2 NVLS (members
  * reduce slices through the switch, store to the root; tolerance), 3 NVLS
  * with the root reducing everything, 4 push with the root's copy pulled by
- * the owners (measured slower; kept for A/B). */
+ * the owners (measured slower; kept for A/B). "wave_lag" (default 2): push
+ * phases with several waves hand out a wave's reducing pieces after the
+ * landing pieces of that many later waves. */
 int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value);
 
 /* NVLS (NVLink SHARP): with RS_NVLS=1 at context creation the heaps are

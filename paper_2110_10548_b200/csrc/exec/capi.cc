@@ -283,10 +283,13 @@ int rs_ctx_set_option(rs_ctx* ctx, const char* key, long long value) {
     ctx->impl->nvls_bcast = value != 0;
   } else if (k == "reduce_push_min_bytes") {
     ctx->impl->reduce_push_min_bytes = value < 0 ? ~0ull : static_cast<uint64_t>(value);
+  } else if (k == "wave_lag") {
+    if (value < 0 || value > 64) return Bad("wave_lag must be in [0, 64]");
+    ctx->impl->wave_lag = static_cast<int>(value);
   } else if (k == "reduce_wave_bytes") {
     ctx->impl->reduce_wave_bytes = value <= 0 ? 0 : (static_cast<uint64_t>(value) & ~15ull);
   } else {
-    return Bad("unknown option (push_min_bytes | barrier_timeout_ms | nvls | nvls_min_group | nvls_min_bytes | ll_max_bytes | ll_total_bytes | nvls_bcast | reduce_mode | reduce_push_min_bytes | reduce_wave_bytes | push_wave_bytes)");
+    return Bad("unknown option (push_min_bytes | barrier_timeout_ms | nvls | nvls_min_group | nvls_min_bytes | ll_max_bytes | ll_total_bytes | nvls_bcast | reduce_mode | reduce_push_min_bytes | reduce_wave_bytes | push_wave_bytes | wave_lag)");
   }
   return RS_OK;
 }

@@ -156,6 +156,7 @@ void ReadTimeoutEnv(Context* ctx) {
   if (const char* env = std::getenv("RS_PUSH_WAVE_BYTES")) {
     ctx->push_wave_bytes = std::strtoull(env, nullptr, 10) & ~15ull;
   }
+  if (const char* env = std::getenv("RS_WAVE_LAG")) ctx->wave_lag = std::max(0, std::atoi(env));
   if (const char* env = std::getenv("RS_REDUCE_MODE")) {
     const int m = std::atoi(env);
     if (m >= kReduceAuto && m <= kReducePushRootPulled) ctx->reduce_mode = m;

@@ -157,6 +157,12 @@ class Context {
   bool nvls_bcast = false;  // measured slower at K=4 (profiles/r02_bcast_nvls_k4.txt): opt-in
   uint64_t reduce_push_min_bytes = 128ull << 20;
   uint64_t reduce_wave_bytes = 4ull << 20;
+  // Push phases with several waves hand out a wave's reducing pieces after
+  // the landing pieces of wave_lag later waves (option "wave_lag", env
+  // RS_WAVE_LAG): the flags a reducing piece waits on are then more often
+  // already set. K=4 Reduce 256 MiB / 512 MiB / 1 GiB: 525 / 958 / 1826 us at
+  // lag 0, 514 / 925 / 1781 at lag 2 (profiles/r02_wave_lag.txt).
+  int wave_lag = 2;
   // One-shot (LL) steps: when every cross-GPU group of a step has its members
   // on distinct GPUs, each GPU sends any peer at most ll_max_bytes and at most
   // ll_total_bytes in total (payload; packets double it), the step runs as

@@ -1075,11 +1075,9 @@ absl::Status CompilePlan(Context* ctx, int num_steps, const int32_t* step_op,
     // cannot deadlock (all CTAs of a launch are resident).
     std::vector<ProtoTask> list = std::move(tasks.a);
     list.insert(list.end(), tasks.b.begin(), tasks.b.end());
-    // RS_WAVE_LAG (A/B): a wave's reducing pieces are handed out after the
-    // landing pieces of `lag` later waves (still deadlock-free: landing
-    // pieces never wait).
-    int lag = 0;
-    if (const char* v = std::getenv("RS_WAVE_LAG")) lag = std::max(0, std::atoi(v));
+    // A wave's reducing pieces are handed out after the landing pieces of
+    // wave_lag later waves (still deadlock-free: landing pieces never wait).
+    const int lag = ctx->wave_lag;
     auto order_key = [&](const ProtoTask& t) {
       if (t.flag_send >= 0) {
         const int from = ctx->slot_rank[t.owner];

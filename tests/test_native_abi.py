@@ -115,5 +115,7 @@ def test_plan_options_validated():
     assert b"piece_queue" in lib.rs_last_error()
     for key in (b"ll_total_bytes", b"reduce_push_min_bytes", b"reduce_wave_bytes", b"push_wave_bytes"):
         assert lib.rs_ctx_set_option(ctx._h, key, 1 << 20) == nat.RS_OK, key
+    assert lib.rs_ctx_set_option(ctx._h, b"wave_lag", 2) == nat.RS_OK
+    assert lib.rs_ctx_set_option(ctx._h, b"wave_lag", -1) == nat.RS_INVALID_ARGUMENT
     plan.close()
     ctx.close()

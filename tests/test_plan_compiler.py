@@ -505,13 +505,14 @@ def test_reduce_auto_policy_by_size():
     assert modes(ctx.compile(prog, (4 << 20) // 2, numeric.BF16).describe()) == {0}
 
 
+@pytest.mark.parametrize("lag", [0, 2])
 @pytest.mark.parametrize("mapping", ["one_per_gpu", "two_gpus", "interleaved2"])
 @pytest.mark.parametrize("reduce_mode", [0, 1])
-def test_push_waves_bit_exact_and_ordered(mapping, reduce_mode):
+def test_push_waves_bit_exact_and_ordered(mapping, reduce_mode, lag):
     """Push waves (push_wave_bytes): parts are cut into waves whose landing
-    tasks precede their reducing tasks and every earlier wave's tasks — the
-    plan stays hazard-free and equal to the oracle; unaligned part edges
-    still pull (scalar tasks only at the true edges)."""
+    tasks precede their reducing tasks (by wave_lag waves) — the plan stays
+    hazard-free and equal to the oracle; unaligned part edges still pull
+    (scalar tasks only at the true edges)."""
     K, progs = golden_programs("cfg2_r01")
     slot_rank, world = MAPPINGS[mapping](K)
     ctx = executor.Context.virtual(K, slot_rank, world)
@@ -520,6 +521,7 @@ def test_push_waves_bit_exact_and_ordered(mapping, reduce_mode):
     ctx.set_option("push_wave_bytes", 16 << 10)
     ctx.set_option("reduce_wave_bytes", 16 << 10)
     ctx.set_option("reduce_mode", reduce_mode)
+    ctx.set_option("wave_lag", lag)
     N = (1 << 17) + 3
     waves = 0
     for _, _, prog, _ in progs[::23]:
@@ -532,7 +534,7 @@ def test_push_waves_bit_exact_and_ordered(mapping, reduce_mode):
                 if len(sends) > 1:
                     waves += 1
                 # interleaved: some reducing task precedes the last landing task
-                if len(sends) > 4 and recvs:
+                if len(sends) > 4 and recvs and lag == 0:
                     assert recvs[0] < sends[-1], modes
                 assert sum(1 for t in rk["tasks"] if not t["vec"]) <= 4 * len(rk["tasks"])
         inputs = numeric.synthetic_inputs(K, N, numeric.BF16)
