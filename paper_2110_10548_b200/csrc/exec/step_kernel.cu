@@ -1119,12 +1119,12 @@ __device__ __forceinline__ void Phase(const StepArgs& a, const uint64_t base, co
     }
     RS_TRACE(3ull * p + 2);
   };
-  // Push phases (a.dynamic): pieces are handed out in launch order through
-  // an atomic counter, so a CTA takes a wave's reducing piece only after
-  // every landing piece of that wave has been taken (no CTA sits on a flag
-  // wait while landing work is left unclaimed; deadlock-free because landing
-  // pieces never wait). Other phases: static grid stride or (below) the
-  // prefetched queue.
+  // Push phases (a.dynamic == 1): pieces are handed out in launch order
+  // through an atomic counter, so a CTA takes a wave's reducing piece only
+  // after every landing piece of that wave (and of wave_lag later waves) has
+  // been taken (no CTA sits on a flag wait while landing work is left
+  // unclaimed; deadlock-free because landing pieces never wait). Other
+  // phases: static grid stride (0) or the prefetched queue (2, below).
   __shared__ uint32_t next_piece;
   auto next = [&](uint32_t p) -> uint32_t {
     if (!a.dynamic) return p + ncta;
