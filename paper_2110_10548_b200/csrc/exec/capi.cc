@@ -343,7 +343,7 @@ int rs_plan_set_option(rs_plan* plan, const char* key, long long value) {
   } else if (k == "push_prefetch") {
     plan->impl->push_prefetch = value != 0;
   } else if (k == "piece_queue") {
-    if (value < 0 || value > 2) return Bad("piece_queue must be 0, 1 or 2");
+    if (value < -1 || value > 2) return Bad("piece_queue must be -1 (auto), 0, 1 or 2");
     plan->impl->piece_queue = static_cast<int>(value);
   } else {
     return Bad("unknown option (unroll | threads | max_ctas | wide_loads | dynamic_pieces | pdl | local_wide | vec256 | remote256 | piece_queue | push_prefetch)");

@@ -240,11 +240,12 @@ class Plan {
   // Phases without chunk flags take their pieces from a prefetched atomic
   // queue instead of a static grid stride (option "piece_queue", env
   // RS_PIECE_QUEUE): 0 never, 1 phases in which the rank touches only its
-  // own HBM (N=1 config 2 2864 -> 3110 GB/s, same DRAM bytes), 2 (default)
-  // also pull phases (same-box ABAB: N=2 1818 -> 1843, N=4 2127 ->
-  // 2151 GB/s, K=4 collectives neutral); only phases with >= 2 pieces per
-  // CTA (profiles/r02_piece_queue.txt).
-  int piece_queue = 2;
+  // own HBM (N=1 config 2 2864 -> 3110 GB/s, same DRAM bytes), 2 also pull
+  // phases (same-box ABAB: N=2 1818 -> 1843, N=4 2127 -> 2151 GB/s, K=4
+  // collectives neutral; emulated 8 ranks on one GPU 1215 -> 1150), -1
+  // (default) 1 plus 2's pull phases on up to 4 real GPUs, where measured.
+  // Only phases with >= 2 pieces per CTA (profiles/r02_piece_queue.txt).
+  int piece_queue = -1;
   // Push phases reserve their next piece ahead too (option "push_prefetch",
   // env RS_PUSH_PREFETCH). Deadlock-free (pieces are still handed out in
   // order, so a CTA holding a reserved landing piece of wave w waits only on

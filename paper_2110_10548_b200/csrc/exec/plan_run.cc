@@ -96,8 +96,11 @@ void BuildLaunches(Plan* plan) {
       // phase of a one-GPU context, the GPU-local steps of multi-GPU ones);
       // 2: also pull phases. NVLS and one-shot phases keep the static stride
       // (NVLS was not A/B'd with the queue).
+      // -1 (auto, default): 1, plus pull phases where that was measured
+      // faster (2 and 4 real GPUs; emulated 8 ranks on one GPU: -5 %).
       const bool own_hbm = rsx.remote_peers == 0;
-      if (a.dynamic == 0 && !a.has_ll && !a.has_nvls && (plan->piece_queue >= 2 || (plan->piece_queue == 1 && own_hbm)))
+      const bool pull_q = plan->piece_queue >= 2 || (plan->piece_queue < 0 && !ctx->emulated && R <= 4);
+      if (a.dynamic == 0 && !a.has_ll && !a.has_nvls && plan->piece_queue != 0 && (own_hbm || pull_q))
         a.dynamic = 2;
       int resident = plan->ctas_per_sm * rank.sm_count;
       if (ctx->emulated) {

@@ -83,10 +83,10 @@ def test_config2_full_size_bf16_local(local8):
         _run(local8, prog, K, N, numeric.BF16, inputs=inputs)
 
 
-@pytest.mark.parametrize("queue", [0, 1, 2])
+@pytest.mark.parametrize("queue", [-1, 0, 1, 2])
 def test_piece_schedules_local(local8, queue):
     """Static grid stride (piece_queue 0) and the prefetched atomic queue
-    (1, 2): the same bytes, bit-exact, replayed (the queue word resets at
+    (-1 auto, 1, 2): the same bytes, bit-exact, replayed (the queue word resets at
     the end of each launch). describe() after a run reports the schedule:
     the queue only on phases with >= 2 pieces per CTA."""
     K, progs = golden_programs("cfg2_r01")

@@ -111,6 +111,7 @@ def test_plan_options_validated():
         assert lib.rs_plan_set_option(plan._h, key, val) == nat.RS_OK, key
     assert lib.rs_plan_set_option(plan._h, b"unroll", 3) == nat.RS_INVALID_ARGUMENT
     assert lib.rs_plan_set_option(plan._h, b"piece_queue", 3) == nat.RS_INVALID_ARGUMENT
+    assert lib.rs_plan_set_option(plan._h, b"piece_queue", -1) == nat.RS_OK
     assert lib.rs_plan_set_option(plan._h, b"bogus", 1) == nat.RS_INVALID_ARGUMENT
     assert b"piece_queue" in lib.rs_last_error()
     for key in (b"ll_total_bytes", b"reduce_push_min_bytes", b"reduce_wave_bytes", b"push_wave_bytes"):
