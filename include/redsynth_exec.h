@@ -212,7 +212,9 @@ int rs_plan_set_launch(rs_plan* plan, int max_ctas, int threads);
  * "piece_queue" (phases without chunk flags take pieces from a prefetched
  * atomic queue: 0 never, 1 phases touching only the rank's own HBM, 2 also
  * pull phases, -1 (default) 1 plus pull phases on up to 4 real GPUs; only
- * phases with >= 2 pieces per CTA, never NVLS or one-shot phases). */
+ * phases with >= 2 pieces per CTA, never NVLS or one-shot phases),
+ * "push_prefetch" (push phases reserve their next piece ahead too; default
+ * 0, measured slower). */
 int rs_plan_set_option(rs_plan* plan, const char* key, long long value);
 
 /* JSON dump of the compiled plan: per step, per rank, the entry-barrier
